@@ -1,0 +1,191 @@
+/*
+ * tide.h -- C ABI of the B200-native TIDE MoE layer-step (arXiv 2605.20179).
+ *
+ * One call, tide_moe_step(), runs one MoE layer at one denoising step for all
+ * tokens of the block(s) at once (Alg. 1):
+ *
+ *   a1 router logits        l = X Wr^T
+ *   a2 softmax + top-k      lowest id wins ties             (R-1..R-4)
+ *   a3 hit histogram        hits[e] = #{(n,j): topk = e}
+ *   a4 refresh + placement  if step % interval == 0:
+ *                           top-`capacity` experts by hits
+ *   a5 buckets              resident first, ascending id    (R-11)
+ *   a6 non-resident I/O     pinned host -> HBM, side stream (R-13)
+ *   a7/a8 grouped SwiGLU    y = Wd (silu(Wg x) * Wu x)      (north_star)
+ *   a9 shared expert        (flag)                          (R-16)
+ *   a10 combine             out[n] = sum_j g[n,j] y[n,j]
+ *
+ * P:n = /root/reference/PAPER.md line n; R-x = a reading in DESIGN.md section 3.
+ *
+ * Conventions
+ *  - Every pointer is owned by the caller unless stated otherwise.  "device"
+ *    pointers are CUDA device (HBM) addresses on the context's device; "host"
+ *    pointers are CPU addresses.
+ *  - `stream` is a cudaStream_t passed as void*; all device work of a call is
+ *    ordered on it and outputs are valid once it completes.
+ *  - Every entry point returns tide_status; no C++ exception crosses the ABI.
+ *    tide_last_error() returns a thread-local message for the last failure.
+ *  - Argument checks run before any work is enqueued; on TIDE_EINVAL /
+ *    TIDE_ECAPACITY / TIDE_EUNSUPPORTED nothing was enqueued.  The one
+ *    exception is TIDE_EPLACEMENT (see tide_moe_step).
+ *  - Asynchronous device faults surface as TIDE_ECUDA at a later call.
+ */
+#ifndef TIDE_H
+#define TIDE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIDE_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TIDE_API __attribute__((visibility("default")))
+#else
+#define TIDE_API
+#endif
+
+typedef enum {
+  TIDE_OK = 0,
+  TIDE_EINVAL = 1,        /* bad argument (null pointer, size out of range)        */
+  TIDE_ECAPACITY = 2,     /* capacity outside [1, E] (or [1, E/P] under EP)        */
+  TIDE_EPLACEMENT = 3,    /* non-refresh step with popcount(placement) > capacity */
+  TIDE_ECUDA = 4,         /* CUDA runtime/driver failure                           */
+  TIDE_ENCCL = 5,         /* NCCL failure (EP)                                     */
+  TIDE_ENOMEM = 6,        /* device or pinned allocation failed                    */
+  TIDE_EUNSUPPORTED = 7   /* shape/flag combination this build does not support    */
+} tide_status;
+
+/* Element type of activations, router weights, expert weights and `out`.   */
+typedef enum { TIDE_F32 = 0, TIDE_BF16 = 1 } tide_dtype;
+
+enum {
+  TIDE_NORM_TOPK = 1u << 0,     /* renormalise the k selected gates (R-2)          */
+  TIDE_SHARED_EXPERT = 1u << 1, /* add one always-resident shared expert (R-16)    */
+  TIDE_LAZY_PROMOTE = 1u << 2   /* copy a promoted expert on its first hit (R-9)   */
+};
+
+/* Shape of one MoE layer.  Constraints checked by tide_ctx_create:
+ *   1 <= top_k <= num_experts <= 1024, hidden and ffn multiples of 64,
+ *   64 <= hidden <= 16384, 64 <= ffn <= 16384, 1 <= max_tokens <= 1024.     */
+typedef struct {
+  int32_t num_experts; /* E                                                   */
+  int32_t top_k;       /* k                                                   */
+  int32_t hidden;      /* model width H                                       */
+  int32_t ffn;         /* expert intermediate width F (shared expert too)     */
+  int32_t max_tokens;  /* largest num_tokens a step will be called with        */
+  tide_dtype dtype;    /* TIDE_BF16 (tcgen05 kind::f16) or TIDE_F32 (kind::tf32) */
+  uint32_t flags;      /* TIDE_NORM_TOPK | TIDE_SHARED_EXPERT | TIDE_LAZY_PROMOTE */
+} tide_layer_desc;
+
+/* Packed expert layout ("pack"): one expert = [Wg (F x H); Wu (F x H); Wd (H x F)],
+ * each row-major, contiguous, 3*H*F elements of `dtype`.  Wg/Wu rows are the
+ * F gate/up projections of the hidden vector, Wd rows the H outputs.      */
+TIDE_API size_t tide_expert_elems(const tide_layer_desc* desc);
+TIDE_API size_t tide_expert_bytes(const tide_layer_desc* desc);
+
+/* Copy one expert's three matrices into packed form at `dst`.  Any of the
+ * pointers may be host or device (unified addressing); the copy is enqueued
+ * on `stream` (cudaMemcpyAsync, cudaMemcpyDefault).                        */
+TIDE_API tide_status tide_pack_expert(const tide_layer_desc* desc, const void* w_gate, const void* w_up,
+                             const void* w_down, void* dst, void* stream);
+
+/* Where the experts' weights live.  Exactly one of device_all / host_master
+ * must be non-NULL.
+ *  device_all : device, E packed experts back to back (no offload: every expert
+ *               is served from HBM; placement is still computed and reported).
+ *  host_master: host, E packed experts back to back, PINNED (cudaHostAlloc or
+ *               cudaHostRegister; checked, else TIDE_EINVAL).  Experts are
+ *               copied into the context's HBM slot pool (capacity slots) and
+ *               staging ring (see tide_ctx_create) as placement and hits demand.
+ *               Must stay valid and unchanged for the lifetime of the context.
+ *  shared_w   : device, one packed expert; required iff TIDE_SHARED_EXPERT.   */
+typedef struct {
+  const void* device_all;
+  const void* host_master;
+  const void* shared_w;
+} tide_expert_weights;
+
+/* Per-step counters (host struct, filled when `stats` is non-NULL; filling it
+ * synchronises `stream`).                                                  */
+typedef struct {
+  int32_t refreshed;          /* step % interval == 0                                    */
+  int32_t resident_pairs;     /* (token, expert) pairs whose expert is in placement'     */
+  int32_t nonresident_pairs;  /* N*k - resident_pairs                                    */
+  int32_t promotions;         /* |placement' \ placement|                                */
+  int32_t evictions;          /* |placement \ placement'|                                */
+  int32_t unique_experts;     /* experts with hits > 0                                   */
+  int32_t experts_streamed;   /* hit experts whose weights were not in HBM at step start */
+  int32_t copies;             /* expert H2D copies enqueued this step (incl. eager promotions) */
+  int64_t h2d_bytes;          /* copies * tide_expert_bytes                              */
+  int64_t weight_bytes_read;  /* expert weight bytes the grouped FFN streamed from HBM   */
+} tide_step_stats;
+
+/* Optional device outputs for tests (nullable members, device pointers).  */
+typedef struct {
+  int32_t* topk_idx; /* [N, k] ranked expert ids                                  */
+  float* gates;      /* [N, k]                                                    */
+  int32_t* pos;      /* [N, k] row of pair (n, j) in bucket order (R-11)          */
+  int32_t* order;    /* [E] expert at each bucket position                        */
+  int32_t* offsets;  /* [E + 1] first row of each bucket position                 */
+  float* logits;     /* [N, E] fp32 router logits                                 */
+} tide_step_debug;
+
+typedef struct tide_ctx tide_ctx;
+
+/* Create a context for one layer on `device`.
+ *  capacity      : C, HBM-resident experts for this layer (1 <= C <= E).  In
+ *                  host_master mode the context owns C HBM slots.
+ *  staging_slots : S >= 2, HBM staging ring for non-resident hits (R-13); the
+ *                  ring is allocated on the first host_master step (S * expert
+ *                  bytes) and is reported as HBM overhead beyond C.
+ * The context owns its workspaces (sized by max_tokens), slot pool, staging
+ * ring, streams and events.  Not thread-safe; distinct contexts may run
+ * concurrently on distinct streams.                                         */
+TIDE_API tide_status tide_ctx_create(const tide_layer_desc* desc, int32_t capacity, int32_t staging_slots,
+                            int32_t device, tide_ctx** out);
+TIDE_API void tide_ctx_destroy(tide_ctx* ctx);
+
+/* One MoE layer-step.
+ *  block_hidden  : device [num_tokens, H] of dtype, the block's hidden states.
+ *  num_tokens    : N, 0 <= N <= max_tokens.
+ *  router_w      : device [E, H] of dtype.
+ *  expert_w      : weights, see tide_expert_weights.
+ *  placement     : device [E] uint8, nonzero = resident (the caller's current
+ *                  placement; at step 0 of a block any value, R-7).
+ *  step          : denoising step within the block, >= 0.
+ *  interval      : refresh interval tau >= 1; refresh iff step % interval == 0.
+ *  capacity      : must equal the context's capacity.
+ *  out           : device [N, H] of dtype.
+ *  hit_counts    : device [E] int32, this step's hits (Sum = N*k).
+ *  placement_out : device [E] uint8, placement' (may alias `placement`).
+ * Returns TIDE_EPLACEMENT when the step is not a refresh and the input
+ * placement holds more than `capacity` experts.  That check runs on the
+ * device: when it fails, the router/routing kernels (and hit_counts) have
+ * run but nothing after them, and `out` / `placement_out` are not written.
+ * In device_all mode (no offload) the check is reported only when `stats`
+ * is requested (the call does not otherwise synchronise).
+ * In host_master mode the call blocks once on an internal event after the
+ * routing kernels to read the <= E-entry miss list, then enqueues H2D copies
+ * on an internal side stream, overlapped with the resident experts' FFN.   */
+TIDE_API tide_status tide_moe_step(tide_ctx* ctx, const void* block_hidden, int32_t num_tokens,
+                          const void* router_w, const tide_expert_weights* expert_w,
+                          const uint8_t* placement, int32_t step, int32_t interval,
+                          int32_t capacity, void* out, int32_t* hit_counts,
+                          uint8_t* placement_out, tide_step_stats* stats, tide_step_debug* dbg,
+                          void* stream);
+
+/* Thread-local description of the last failure on this thread. */
+TIDE_API const char* tide_last_error(void);
+
+/* ABI version (TIDE_ABI_VERSION) and the device kernels' SM target (100). */
+TIDE_API int32_t tide_abi_version(void);
+TIDE_API int32_t tide_build_sm(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIDE_H */

@@ -245,8 +245,10 @@ int orc_moe_step(const orc_layer* L, int N, const void* x, const void* wr,
 }
 
 /* ---------------- O10: I/O model (Alg. 1 lines 3-4) ----------
- * R-12: weights are read-only, eviction frees a slot (no D2H copy).
- * R-13: a hit expert that is not loaded is copied host->HBM; if it is in
+ * R-12: weights are read-only; eviction frees a slot (no D2H copy) and takes
+ * effect after this step's compute, so an expert whose weights are in HBM at
+ * the start of the step is served from HBM this step.
+ * R-13: a hit expert that is not in HBM is copied host->HBM; if it is in
  * the new resident set it keeps its slot, otherwise it is streamed into
  * staging for this step only.  R-9: with lazy=0 a promoted expert is
  * copied at the refresh even without hits this step.                   */
@@ -260,16 +262,16 @@ int orc_io_step(int E, int lazy, const int32_t* hits, const uint8_t* placement_i
     if (now) io->resident_pairs += hits[e];
     else io->nonresident_pairs += hits[e];
   }
-  for (int e = 0; e < E; ++e) /* evicted (or never placed) experts lose their slot */
-    if (!placement_out[e]) loaded[e] = 0;
   for (int e = 0; e < E; ++e) {
+    int kept = 0;
     if (hits[e] > 0 && !loaded[e]) io->experts_streamed++;
     if (placement_out[e] && !loaded[e] && (!lazy || hits[e] > 0)) {
-      io->copies++;
-      loaded[e] = 1;
-    } else if (!placement_out[e] && hits[e] > 0) {
+      io->copies++; /* copied into a slot and retained */
+      kept = 1;
+    } else if (!placement_out[e] && hits[e] > 0 && !loaded[e]) {
       io->copies++; /* staged for this step, not retained */
     }
+    loaded[e] = (uint8_t)((loaded[e] && placement_out[e]) || kept);
   }
   return 0;
 }

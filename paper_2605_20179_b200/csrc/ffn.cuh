@@ -1,0 +1,295 @@
+// ffn.cuh -- a7/a8/a9: grouped SwiGLU expert FFN on tcgen05 tensor cores fed by TMA.
+//
+//   phase 1 (per work entry w, F-tile t):  u = Wg[t] X_w^T, v = Wu[t] X_w^T   (TMEM, fp32)
+//                                          h[w, t] = bf16(silu(u) * v)         (R-14)
+//   phase 2 (per entry w, H-tile t):       y[w, t] = Wd[t] h_w^T                (TMEM -> fp32 y)
+//
+// The expert weights are the MMA M operand (128 rows per tile, streamed once per
+// work entry, L2 evict-first); the entry's tokens are the N operand (m <= 128
+// rows, padded to a multiple of 16, L2 evict-last).  Because m is small the
+// kernel is a weight stream: it is judged by HBM GB/s.
+//
+// Persistent, warp-specialised, one CTA per SM (192 threads):
+//   warp 0 lane 0 : scheduler + TMA producer (global atomic work counter; items are
+//                   all phase-1 items in entry order, then all phase-2 items)
+//   warp 1 lane 0 : tcgen05.mma issuer (single thread), commits to mbarriers
+//   warps 2..5    : epilogue (TMEM -> registers -> global); warp 2 owns TMEM alloc
+// A phase-2 item waits (acquire) on its entry's phase-1 counter; phase-1 items are
+// all claimed before any phase-2 item, so the wait cannot deadlock.
+#pragma once
+#include <type_traits>
+
+#include "ptx.cuh"
+#include "route.cuh"
+
+namespace tide {
+
+constexpr int kFfnThreads = 192;
+constexpr int kStages = 4;
+constexpr int kItemSlots = 4;
+constexpr int kTileM = 128;
+constexpr int kATile = kTileM * 128;           // 16 KB: 128 rows x 128 B (one K block)
+constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 128 B
+constexpr int kStageBytes = 2 * kATile + kBTile;
+constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048;
+
+struct FfnParams {
+  CUtensorMap map_gu;    // routed pool viewed as rows of H elements (gate/up rows)
+  CUtensorMap map_d;     // routed pool viewed as rows of F elements (down rows)
+  CUtensorMap map_gu_s;  // shared expert, rows of H
+  CUtensorMap map_d_s;   // shared expert, rows of F
+  CUtensorMap map_x;     // X_perm [rows, H]
+  CUtensorMap map_h;     // h_perm [rows, F]
+  const int4* entries;   // {slot, row offset, tokens, flags(bit0 = shared)}
+  const int* n_entries;
+  int* sched;
+  int* done;
+  void* h_out;
+  float* y_out;
+  int H, F;
+};
+
+struct FfnItem {
+  int kind;  // 0 gate/up, 1 down, -1 end
+  int tile, slot, off, m, flags, entry, pad;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kFfnThreads, 1)
+    tide_ffn_kernel(const __grid_constant__ FfnParams p) {
+  constexpr bool kTF32 = std::is_same<T, float>::value;
+  constexpr int EB = sizeof(T);
+  constexpr int BK = 128 / EB;  // elements per K block (one 128-byte swizzle row)
+  constexpr int UK = 32 / EB;   // elements per MMA K step
+  constexpr int KSTEPS = BK / UK;
+
+  extern __shared__ uint8_t ffn_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(ffn_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ifull = tempty + 2;
+  uint64_t* iempty = ifull + kItemSlots;
+  FfnItem* items = reinterpret_cast<FfnItem*>(iempty + kItemSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(items + kItemSlots);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.H, F = p.F;
+  const int FT = (F + kTileM - 1) / kTileM, HT = (H + kTileM - 1) / kTileM;
+  const int KB1 = H / BK, KB2 = F / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int i = 0; i < kItemSlots; ++i) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], 5); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&p.map_gu);
+    tma_prefetch_desc(&p.map_d);
+    tma_prefetch_desc(&p.map_x);
+    tma_prefetch_desc(&p.map_h);
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ===================== scheduler + TMA producer =====================
+    const int n_ent = *p.n_entries;
+    const int n1 = n_ent * FT, total = n1 + n_ent * HT;
+    const uint64_t pol_w = policy_evict_first(), pol_a = policy_evict_last();
+    int stage = 0, islot = 0;
+    uint32_t sphase = 0, iphase = 0;
+    while (true) {
+      const int it = atomicAdd(p.sched, 1);
+      FfnItem item;
+      item.kind = -1;
+      if (it < total) {
+        int entry, tile;
+        if (it < n1) { item.kind = 0; entry = it / FT; tile = it % FT; }
+        else { item.kind = 1; entry = (it - n1) / HT; tile = (it - n1) % HT; }
+        const int4 en = p.entries[entry];
+        item.tile = tile; item.slot = en.x; item.off = en.y; item.m = en.z; item.flags = en.w;
+        item.entry = entry;
+      }
+      mbar_wait(&iempty[islot], iphase ^ 1);
+      items[islot] = item;
+      mbar_arrive(&ifull[islot]);
+      if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
+      if (item.kind < 0) break;
+      const int nbox = (item.m + 15) >> 4;
+      if (item.kind == 0) {
+        const CUtensorMap* ma = (item.flags & 1) ? &p.map_gu_s : &p.map_gu;
+        const int rowg = item.slot * 3 * F + item.tile * kTileM;
+        const int rowu = rowg + F;
+        for (int kb = 0; kb < KB1; ++kb) {
+          mbar_wait(&empty[stage], sphase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + 2 * kATile;
+          mbar_arrive_expect_tx(&full[stage], 2 * kATile + nbox * 2048);
+          tma_load_2d(sa, ma, &full[stage], kb * BK, rowg, pol_w);
+          tma_load_2d(sa + kATile, ma, &full[stage], kb * BK, rowu, pol_w);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sb + b * 2048, &p.map_x, &full[stage], kb * BK, item.off + 16 * b, pol_a);
+          if (++stage == kStages) { stage = 0; sphase ^= 1; }
+        }
+      } else {
+        // h of this entry must be complete (all FT phase-1 tiles, possibly on other SMs)
+        const int* dp = p.done + item.entry;
+        if (ld_acquire_gpu(dp) < FT) {
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire_gpu(dp) < FT) {
+            __nanosleep(64);
+            if (globaltimer_ns() - t0 > 4000000000ull) {
+              printf("tide: ffn dependency watchdog entry %d\n", item.entry);
+              __trap();
+            }
+          }
+        }
+        fence_proxy_async_global();
+        const CUtensorMap* ma = (item.flags & 1) ? &p.map_d_s : &p.map_d;
+        const int rowd = item.slot * 3 * H + 2 * H + item.tile * kTileM;
+        const bool dual = item.m <= 64;
+        for (int kb = 0; kb < KB2; kb += dual ? 2 : 1) {
+          const int nk = (dual && kb + 1 < KB2) ? 2 : 1;
+          mbar_wait(&empty[stage], sphase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + 2 * kATile;
+          mbar_arrive_expect_tx(&full[stage], nk * (kATile + nbox * 2048));
+          for (int q = 0; q < nk; ++q) {
+            tma_load_2d(sa + q * kATile, ma, &full[stage], (kb + q) * BK, rowd, pol_w);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sb + (q * nbox + b) * 2048, &p.map_h, &full[stage], (kb + q) * BK,
+                          item.off + 16 * b, pol_a);
+          }
+          if (++stage == kStages) { stage = 0; sphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===================== MMA issuer (one thread) =====================
+    int stage = 0, islot = 0, acc = 0;
+    uint32_t sphase = 0, iphase = 0, aphase = 0;
+    while (true) {
+      mbar_wait(&ifull[islot], iphase);
+      const FfnItem item = items[islot];
+      mbar_arrive(&iempty[islot]);
+      if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
+      if (item.kind < 0) break;
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      tc_fence_after();
+      const int nbox = (item.m + 15) >> 4;
+      const uint32_t idesc = idesc_m128((uint32_t)nbox * 16u, kTF32);
+      const uint32_t dcol = tmem + (uint32_t)acc * 256u;
+      if (item.kind == 0) {
+        for (int kb = 0; kb < KB1; ++kb) {
+          mbar_wait(&full[stage], sphase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint64_t dg = smem_desc_sw128(sa), du = smem_desc_sw128(sa + kATile);
+          const uint64_t db = smem_desc_sw128(sa + 2 * kATile);
+#pragma unroll
+          for (int k = 0; k < KSTEPS; ++k) {
+            const uint32_t accum = (kb | k) != 0;
+            tc_mma<kTF32>(dcol, dg + 2 * k, db + 2 * k, idesc, accum);
+            tc_mma<kTF32>(dcol + 128, du + 2 * k, db + 2 * k, idesc, accum);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; sphase ^= 1; }
+        }
+      } else {
+        const bool dual = item.m <= 64;
+        for (int kb = 0; kb < KB2; kb += dual ? 2 : 1) {
+          const int nk = (dual && kb + 1 < KB2) ? 2 : 1;
+          mbar_wait(&full[stage], sphase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          for (int q = 0; q < nk; ++q) {
+            const uint64_t da = smem_desc_sw128(sa + q * kATile);
+            const uint64_t db = smem_desc_sw128(sa + 2 * kATile + q * nbox * 2048);
+#pragma unroll
+            for (int k = 0; k < KSTEPS; ++k)
+              tc_mma<kTF32>(dcol, da + 2 * k, db + 2 * k, idesc, ((kb + q) | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; sphase ^= 1; }
+        }
+      }
+      tc_commit(&tfull[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  } else if (warp >= 2) {
+    // ===================== epilogue (4 warps, one TMEM lane quarter each) =====================
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    int islot = 0, acc = 0;
+    uint32_t iphase = 0, aphase = 0;
+    while (true) {
+      mbar_wait(&ifull[islot], iphase);
+      const FfnItem item = items[islot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&iempty[islot]);
+      if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
+      if (item.kind < 0) break;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)acc * 256u;
+      if (item.kind == 0) {
+        const int f = item.tile * kTileM + row;
+        T* hcol = reinterpret_cast<T*>(p.h_out) + f;
+        for (int c0 = 0; c0 < item.m; c0 += 16) {
+          float g[16], u[16];
+          tmem_ld16(tbase + c0, g);
+          tmem_ld16(tbase + 128 + c0, u);
+          if (f < F) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (c0 + i < item.m) {
+                const float s = g[i] / (1.0f + __expf(-g[i]));
+                hcol[(size_t)(item.off + c0 + i) * F] = from_f32<T>(s * u[i]);
+              }
+            }
+          }
+        }
+      } else {
+        const int h = item.tile * kTileM + row;
+        float* ycol = p.y_out + h;
+        for (int c0 = 0; c0 < item.m; c0 += 16) {
+          float v[16];
+          tmem_ld16(tbase + c0, v);
+          if (h < H) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < item.m) ycol[(size_t)(item.off + c0 + i) * H] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+      if (item.kind == 0) {  // publish this F-tile of h to phase-2 consumers on any SM
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) red_release_gpu_add(p.done + item.entry, 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace tide

@@ -1,0 +1,667 @@
+// tide.cu -- host runtime + C ABI (include/tide.h) of the TIDE MoE layer-step.
+//
+// One tide_ctx per (layer, device).  It owns the workspaces, the HBM slot pool
+// (capacity experts) and staging ring for host_master mode, the side stream used
+// for H2D expert copies, events, and cached TMA tensor maps.  The host side of
+// a step is: validate -> router -> route -> gather -> FFN over experts already
+// in HBM -> [host_master: read the miss list, enqueue H2D copies on the side
+// stream, FFN over each staged chunk once its copy event fires] -> combine.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tide.h"
+#include "ffn.cuh"
+#include "route.cuh"
+
+using namespace tide;
+
+namespace {
+
+thread_local std::string g_err;
+
+tide_status fail(tide_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CU_TRY(expr)                                                                     \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(TIDE_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major [rows, cols] matrix; box = (128 B of columns) x box_rows,
+// 128-byte swizzle (matches smem_desc_sw128).
+tide_status make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t cols, uint64_t rows,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(TIDE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint32_t eb = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * eb};
+  cuuint32_t box[2] = {128u / eb, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TIDE_ECUDA, "cuTensorMapEncodeTiled failed (%d) cols=%llu rows=%llu", (int)r,
+                (unsigned long long)cols, (unsigned long long)rows);
+  return TIDE_OK;
+}
+
+}  // namespace
+
+struct tide_ctx {
+  tide_layer_desc d;
+  int capacity = 0, staging = 0, device = 0, num_sms = 148;
+  int E = 0, k = 0, H = 0, F = 0, maxN = 0;
+  bool bf16 = true;
+  size_t eb = 2, expert_elems = 0, expert_bytes = 0;
+  int max_rows = 0, max_entries = 0;
+
+  // workspaces (device)
+  float* logits = nullptr;
+  int* topk = nullptr;
+  float* gates = nullptr;
+  int* pos = nullptr;
+  int* order = nullptr;
+  int* offsets = nullptr;
+  void* x_perm = nullptr;
+  void* h_perm = nullptr;
+  float* y_perm = nullptr;
+  int4* entries = nullptr;
+  int* done = nullptr;
+  RouteInfo* info = nullptr;  // + 4E ints + E bytes
+  size_t info_bytes = 0;
+  int* slot_of_dev = nullptr;
+
+  // host_master mode
+  void* pool = nullptr;            // (capacity + staging) packed experts
+  int4* entries2 = nullptr;        // staged-chunk work lists (device)
+  int* ctrl2 = nullptr;            // per chunk {n_entries, sched}
+  int* done2 = nullptr;
+  int max_chunks = 0, max_entries2 = 0;
+  void* h_info = nullptr;          // pinned mirror of info block
+  int4* h_entries2 = nullptr;      // pinned
+  int* h_ctrl2 = nullptr;          // pinned (ctrl2 + done2 zeros)
+  int* h_slot_of = nullptr;        // pinned mirror of slot_of_dev
+  std::vector<int> slot_of;        // expert -> pool slot (authoritative)
+  std::vector<int> owner;          // pool slot -> expert (-1 free)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_info = nullptr, ev_gemm1 = nullptr, ev_side_done = nullptr;
+  std::vector<cudaEvent_t> ev_chunk_ready, ev_chunk_done;
+
+  // cached tensor maps
+  CUtensorMap map_x, map_h, map_gu, map_d, map_gu_s, map_d_s;
+  const void* map_src = nullptr;
+  int map_src_rows = 0;
+  const void* map_shared_src = nullptr;
+  bool have_shared_map = false;
+};
+
+extern "C" {
+
+int32_t tide_abi_version(void) { return TIDE_ABI_VERSION; }
+int32_t tide_build_sm(void) { return 100; }
+const char* tide_last_error(void) { return g_err.c_str(); }
+
+size_t tide_expert_elems(const tide_layer_desc* d) {
+  return d ? (size_t)3 * d->hidden * d->ffn : 0;
+}
+size_t tide_expert_bytes(const tide_layer_desc* d) {
+  return d ? tide_expert_elems(d) * (d->dtype == TIDE_BF16 ? 2 : 4) : 0;
+}
+
+tide_status tide_pack_expert(const tide_layer_desc* d, const void* wg, const void* wu,
+                             const void* wd, void* dst, void* stream) {
+  if (!d || !wg || !wu || !wd || !dst) return fail(TIDE_EINVAL, "tide_pack_expert: null argument");
+  const size_t mb = (size_t)d->hidden * d->ffn * (d->dtype == TIDE_BF16 ? 2 : 4);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* o = static_cast<uint8_t*>(dst);
+  CU_TRY(cudaMemcpyAsync(o, wg, mb, cudaMemcpyDefault, s));
+  CU_TRY(cudaMemcpyAsync(o + mb, wu, mb, cudaMemcpyDefault, s));
+  CU_TRY(cudaMemcpyAsync(o + 2 * mb, wd, mb, cudaMemcpyDefault, s));
+  return TIDE_OK;
+}
+
+static tide_status validate_desc(const tide_layer_desc* d) {
+  if (!d) return fail(TIDE_EINVAL, "desc is null");
+  if (d->num_experts < 1 || d->num_experts > 1024)
+    return fail(TIDE_EUNSUPPORTED, "num_experts %d outside [1, 1024]", d->num_experts);
+  if (d->top_k < 1 || d->top_k > d->num_experts || d->top_k > 32)
+    return fail(TIDE_EINVAL, "top_k %d outside [1, min(E, 32)]", d->top_k);
+  if (d->hidden < 64 || d->hidden > 16384 || d->hidden % 64)
+    return fail(TIDE_EUNSUPPORTED, "hidden %d must be a multiple of 64 in [64, 16384]", d->hidden);
+  if (d->ffn < 64 || d->ffn > 16384 || d->ffn % 64)
+    return fail(TIDE_EUNSUPPORTED, "ffn %d must be a multiple of 64 in [64, 16384]", d->ffn);
+  if (d->max_tokens < 1 || d->max_tokens > 1024)
+    return fail(TIDE_EUNSUPPORTED, "max_tokens %d outside [1, 1024]", d->max_tokens);
+  if (d->dtype != TIDE_BF16 && d->dtype != TIDE_F32)
+    return fail(TIDE_EUNSUPPORTED, "dtype %d", (int)d->dtype);
+  return TIDE_OK;
+}
+
+void tide_ctx_destroy(tide_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->side) cudaStreamSynchronize(c->side);
+  void* dev[] = {c->logits, c->topk,  c->gates,    c->pos,   c->order, c->offsets,
+                 c->x_perm, c->h_perm, c->y_perm,  c->entries, c->done, c->info,
+                 c->slot_of_dev, c->pool, c->entries2, c->ctrl2, c->done2};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
+  for (void* p : host)
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : c->ev_chunk_ready) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_chunk_done) cudaEventDestroy(e);
+  if (c->ev_info) cudaEventDestroy(c->ev_info);
+  if (c->ev_gemm1) cudaEventDestroy(c->ev_gemm1);
+  if (c->ev_side_done) cudaEventDestroy(c->ev_side_done);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
+}
+
+#define ALLOC(ptr, bytes)                                                                  \
+  do {                                                                                     \
+    if (cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes)) != cudaSuccess) {           \
+      tide_ctx_destroy(c);                                                                 \
+      return fail(TIDE_ENOMEM, "cudaMalloc(%zu) failed for " #ptr, (size_t)(bytes));        \
+    }                                                                                      \
+    cudaMemset((ptr), 0, (bytes));                                                         \
+  } while (0)
+
+tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t staging_slots,
+                            int32_t device, tide_ctx** out) {
+  if (!out) return fail(TIDE_EINVAL, "out is null");
+  *out = nullptr;
+  tide_status s = validate_desc(d);
+  if (s != TIDE_OK) return s;
+  if (capacity < 1 || capacity > d->num_experts)
+    return fail(TIDE_ECAPACITY, "capacity %d outside [1, %d]", capacity, d->num_experts);
+  if (staging_slots < 2) return fail(TIDE_EINVAL, "staging_slots %d < 2", staging_slots);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(TIDE_ECUDA, "no CUDA device %d", device);
+  CU_TRY(cudaSetDevice(device));
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) return fail(TIDE_EUNSUPPORTED, "device %d is sm_%d0, this build is sm_100a", device, major);
+
+  tide_ctx* c = new tide_ctx();
+  c->d = *d;
+  c->capacity = capacity;
+  c->staging = staging_slots;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  c->E = d->num_experts;
+  c->k = d->top_k;
+  c->H = d->hidden;
+  c->F = d->ffn;
+  c->maxN = d->max_tokens;
+  c->bf16 = d->dtype == TIDE_BF16;
+  c->eb = c->bf16 ? 2 : 4;
+  c->expert_elems = tide_expert_elems(d);
+  c->expert_bytes = tide_expert_bytes(d);
+  const int E = c->E, k = c->k, N = c->maxN;
+  c->max_rows = N * k + N;
+  c->max_entries = E + (N * k) / kMaxTok + 2 + (N + kMaxTok - 1) / kMaxTok;
+
+  ALLOC(c->logits, sizeof(float) * N * E);
+  ALLOC(c->topk, sizeof(int) * N * k);
+  ALLOC(c->gates, sizeof(float) * N * k);
+  ALLOC(c->pos, sizeof(int) * N * k);
+  ALLOC(c->order, sizeof(int) * E);
+  ALLOC(c->offsets, sizeof(int) * (E + 1));
+  ALLOC(c->x_perm, c->eb * (size_t)c->max_rows * c->H);
+  ALLOC(c->h_perm, c->eb * (size_t)c->max_rows * c->F);
+  ALLOC(c->y_perm, sizeof(float) * (size_t)c->max_rows * c->H);
+  ALLOC(c->entries, sizeof(int4) * c->max_entries);
+  ALLOC(c->done, sizeof(int) * c->max_entries);
+  c->info_bytes = sizeof(RouteInfo) + sizeof(int) * 4 * E + E;
+  ALLOC(c->info, c->info_bytes);
+  ALLOC(c->slot_of_dev, sizeof(int) * E);
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_info, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_gemm1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess) {
+    tide_ctx_destroy(c);
+    return fail(TIDE_ECUDA, "stream/event creation failed");
+  }
+  if (make_map(&c->map_x, c->x_perm, c->bf16, c->H, c->max_rows, 16) != TIDE_OK ||
+      make_map(&c->map_h, c->h_perm, c->bf16, c->F, c->max_rows, 16) != TIDE_OK) {
+    std::string m = g_err;
+    tide_ctx_destroy(c);
+    return fail(TIDE_ECUDA, "%s", m.c_str());
+  }
+  // kernel attributes (idempotent)
+  const size_t router_smem = (size_t)kRouterWarps * c->H * c->eb;
+  if (c->bf16) {
+    cudaFuncSetAttribute(tide_router_kernel<__nv_bfloat16>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)router_smem);
+    cudaFuncSetAttribute(tide_ffn_kernel<__nv_bfloat16>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kFfnSmemBytes);
+  } else {
+    cudaFuncSetAttribute(tide_router_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)router_smem);
+    cudaFuncSetAttribute(tide_ffn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kFfnSmemBytes);
+  }
+  const size_t route_smem = sizeof(int) * (4 * E + E * ((N + 31) / 32));
+  cudaFuncSetAttribute(tide_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)route_smem);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    tide_ctx_destroy(c);
+    return fail(TIDE_ECUDA, "ctx init: %s", cudaGetErrorString(e));
+  }
+  c->slot_of.assign(E, -1);
+  *out = c;
+  return TIDE_OK;
+}
+
+// Lazily set up host_master resources (slot pool, staging ring, pinned mirrors).
+static tide_status ensure_pool(tide_ctx* c) {
+  if (c->pool) return TIDE_OK;
+  const int slots = c->capacity + c->staging;
+  if (cudaMalloc(&c->pool, c->expert_bytes * slots) != cudaSuccess)
+    return fail(TIDE_ENOMEM, "slot pool of %d experts (%zu B) failed", slots,
+                c->expert_bytes * slots);
+  c->owner.assign(slots, -1);
+  const int E = c->E;
+  c->max_chunks = E + 2;
+  c->max_entries2 = E + (c->maxN * c->k) / kMaxTok + 2;
+  CU_TRY(cudaMalloc(&c->entries2, sizeof(int4) * c->max_entries2));
+  CU_TRY(cudaMalloc(&c->ctrl2, sizeof(int) * 2 * c->max_chunks));
+  CU_TRY(cudaMalloc(&c->done2, sizeof(int) * c->max_entries2));
+  CU_TRY(cudaHostAlloc(&c->h_info, c->info_bytes, cudaHostAllocDefault));
+  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_entries2), sizeof(int4) * c->max_entries2,
+                       cudaHostAllocDefault));
+  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ctrl2),
+                       sizeof(int) * (2 * c->max_chunks + c->max_entries2), cudaHostAllocDefault));
+  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_slot_of), sizeof(int) * E,
+                       cudaHostAllocDefault));
+  for (int i = 0; i < E; ++i) c->h_slot_of[i] = -1;
+  CU_TRY(cudaMemcpy(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice));
+  c->ev_chunk_ready.resize(c->max_chunks);
+  c->ev_chunk_done.resize(c->max_chunks);
+  for (int i = 0; i < c->max_chunks; ++i) {
+    CU_TRY(cudaEventCreateWithFlags(&c->ev_chunk_ready[i], cudaEventDisableTiming));
+    CU_TRY(cudaEventCreateWithFlags(&c->ev_chunk_done[i], cudaEventDisableTiming));
+  }
+  return TIDE_OK;
+}
+
+static tide_status launch_ffn(tide_ctx* c, const int4* entries, const int* n_entries, int* sched,
+                              int* done, cudaStream_t st) {
+  FfnParams p;
+  p.map_gu = c->map_gu;
+  p.map_d = c->map_d;
+  p.map_gu_s = c->have_shared_map ? c->map_gu_s : c->map_gu;
+  p.map_d_s = c->have_shared_map ? c->map_d_s : c->map_d;
+  p.map_x = c->map_x;
+  p.map_h = c->map_h;
+  p.entries = entries;
+  p.n_entries = n_entries;
+  p.sched = sched;
+  p.done = done;
+  p.h_out = c->h_perm;
+  p.y_out = c->y_perm;
+  p.H = c->H;
+  p.F = c->F;
+  if (c->bf16)
+    tide_ffn_kernel<__nv_bfloat16><<<c->num_sms, kFfnThreads, kFfnSmemBytes, st>>>(p);
+  else
+    tide_ffn_kernel<float><<<c->num_sms, kFfnThreads, kFfnSmemBytes, st>>>(p);
+  CU_TRY(cudaGetLastError());
+  return TIDE_OK;
+}
+
+static tide_status ensure_weight_maps(tide_ctx* c, const void* src, int rows_experts,
+                                      const void* shared) {
+  if (src != c->map_src || rows_experts != c->map_src_rows) {
+    tide_status s = make_map(&c->map_gu, src, c->bf16, c->H, (uint64_t)rows_experts * 3 * c->F, 128);
+    if (s != TIDE_OK) return s;
+    s = make_map(&c->map_d, src, c->bf16, c->F, (uint64_t)rows_experts * 3 * c->H, 128);
+    if (s != TIDE_OK) return s;
+    c->map_src = src;
+    c->map_src_rows = rows_experts;
+  }
+  if (shared && shared != c->map_shared_src) {
+    tide_status s = make_map(&c->map_gu_s, shared, c->bf16, c->H, (uint64_t)3 * c->F, 128);
+    if (s != TIDE_OK) return s;
+    s = make_map(&c->map_d_s, shared, c->bf16, c->F, (uint64_t)3 * c->H, 128);
+    if (s != TIDE_OK) return s;
+    c->map_shared_src = shared;
+    c->have_shared_map = true;
+  }
+  return TIDE_OK;
+}
+
+static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int copies, int entries_total,
+                       tide_step_stats* st) {
+  st->refreshed = info->refreshed;
+  st->resident_pairs = info->resident_pairs;
+  st->nonresident_pairs = N * c->k - info->resident_pairs;
+  st->promotions = info->promotions;
+  st->evictions = info->evictions;
+  st->unique_experts = info->unique_experts;
+  st->experts_streamed = info->n_miss;
+  st->copies = copies;
+  st->h2d_bytes = (int64_t)copies * (int64_t)c->expert_bytes;
+  st->weight_bytes_read = (int64_t)entries_total * (int64_t)c->expert_bytes;
+}
+
+tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
+                          const tide_expert_weights* w, const uint8_t* placement, int32_t step,
+                          int32_t interval, int32_t capacity, void* out, int32_t* hit_counts,
+                          uint8_t* placement_out, tide_step_stats* stats, tide_step_debug* dbg,
+                          void* stream) {
+  // ---------------- argument checks (nothing enqueued on failure)
+  if (!c) return fail(TIDE_EINVAL, "ctx is null");
+  if (N < 0 || N > c->maxN) return fail(TIDE_EINVAL, "num_tokens %d outside [0, %d]", N, c->maxN);
+  if (!w) return fail(TIDE_EINVAL, "expert_w is null");
+  if ((w->device_all == nullptr) == (w->host_master == nullptr))
+    return fail(TIDE_EINVAL, "exactly one of device_all / host_master must be set");
+  const bool shared = (c->d.flags & TIDE_SHARED_EXPERT) != 0;
+  if (shared && !w->shared_w) return fail(TIDE_EINVAL, "TIDE_SHARED_EXPERT set but shared_w is null");
+  if (!placement || !placement_out || !hit_counts || (N > 0 && (!x || !out)) || !wr)
+    return fail(TIDE_EINVAL, "null tensor argument");
+  if (interval < 1) return fail(TIDE_EINVAL, "interval %d < 1", interval);
+  if (step < 0) return fail(TIDE_EINVAL, "step %d < 0", step);
+  if (capacity != c->capacity)
+    return fail(TIDE_ECAPACITY, "capacity %d != context capacity %d", capacity, c->capacity);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU_TRY(cudaSetDevice(c->device));
+  const bool pool_mode = w->host_master != nullptr;
+  if (pool_mode) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, w->host_master) != cudaSuccess ||
+        a.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return fail(TIDE_EINVAL, "host_master is not pinned host memory");
+    }
+    tide_status s = ensure_pool(c);
+    if (s != TIDE_OK) return s;
+  }
+  const int E = c->E, k = c->k, H = c->H;
+  const int refresh = (step % interval) == 0;
+  tide_status s = ensure_weight_maps(c, pool_mode ? c->pool : w->device_all,
+                                     pool_mode ? c->capacity + c->staging : E,
+                                     shared ? w->shared_w : nullptr);
+  if (s != TIDE_OK) return s;
+
+  // ---------------- a1 router
+  if (N > 0) {
+    dim3 grid((E + kRouterWarps - 1) / kRouterWarps, (N + kRouterTokens - 1) / kRouterTokens);
+    const size_t sm = (size_t)kRouterWarps * H * c->eb;
+    if (c->bf16)
+      tide_router_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
+          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wr), c->logits,
+          N, E, H);
+    else
+      tide_router_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(x),
+                                                       static_cast<const float*>(wr), c->logits,
+                                                       N, E, H);
+    CU_TRY(cudaGetLastError());
+  }
+  // ---------------- a2..a5 route
+  RouteParams rp;
+  rp.logits = c->logits;
+  rp.placement_in = placement;
+  rp.slot_of = pool_mode ? c->slot_of_dev : nullptr;
+  rp.N = N;
+  rp.E = E;
+  rp.k = k;
+  rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
+  rp.refresh = refresh;
+  rp.capacity = capacity;
+  rp.shared = shared ? 1 : 0;
+  rp.topk_idx = c->topk;
+  rp.gates = c->gates;
+  rp.pos = c->pos;
+  rp.order = c->order;
+  rp.offsets = c->offsets;
+  rp.hit_counts = hit_counts;
+  rp.placement_out = placement_out;
+  rp.info = c->info;
+  rp.entries = c->entries;
+  rp.done = c->done;
+  const size_t route_smem = sizeof(int) * (4 * E + E * ((N + 31) / 32));
+  tide_route_kernel<<<1, kRouteThreads, route_smem, st>>>(rp);
+  CU_TRY(cudaGetLastError());
+  if (pool_mode) {
+    CU_TRY(cudaMemcpyAsync(c->h_info, c->info, c->info_bytes, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaEventRecord(c->ev_info, st));
+  }
+  // ---------------- a5 gather, a7 FFN over experts already in HBM (+ shared)
+  if (N > 0) {
+    if (c->bf16)
+      tide_gather_kernel<__nv_bfloat16><<<N, 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), c->pos, c->info,
+          static_cast<__nv_bfloat16*>(c->x_perm), N, k, H, shared ? 1 : 0);
+    else
+      tide_gather_kernel<float><<<N, 256, 0, st>>>(static_cast<const float*>(x), c->pos, c->info,
+                                                   static_cast<float*>(c->x_perm), N, k, H,
+                                                   shared ? 1 : 0);
+    CU_TRY(cudaGetLastError());
+    s = launch_ffn(c, c->entries, &c->info->n_entries, &c->info->sched, c->done, st);
+    if (s != TIDE_OK) return s;
+  }
+
+  int copies = 0, staged_entries = 0;
+  const RouteInfo* hinfo = nullptr;
+  if (pool_mode) {
+    CU_TRY(cudaEventRecord(c->ev_gemm1, st));
+    CU_TRY(cudaEventSynchronize(c->ev_info));
+    hinfo = static_cast<const RouteInfo*>(c->h_info);
+    if (hinfo->status != 0)
+      return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
+                  step, capacity);
+    const int* hi = reinterpret_cast<const int*>(hinfo + 1);
+    const int* miss_e = hi;
+    const int* miss_off = miss_e + E;
+    const int* miss_m = miss_off + E;
+    const int* hits = miss_m + E;
+    const uint8_t* pl = reinterpret_cast<const uint8_t*>(hits + E);
+    const bool lazy = (c->d.flags & TIDE_LAZY_PROMOTE) != 0;
+    const int C = c->capacity, S = c->staging, half = std::max(1, S / 2);
+    const uint8_t* master = static_cast<const uint8_t*>(w->host_master);
+    uint8_t* pool = static_cast<uint8_t*>(c->pool);
+    const size_t xb = c->expert_bytes;
+
+    // release slots of experts that left the resident set (R-12: no D2H)
+    std::vector<int> free_now, free_after_gemm1;
+    for (int sl = 0; sl < C; ++sl)
+      if (c->owner[sl] < 0) free_now.push_back(sl);
+    for (int e = 0; e < E; ++e) {
+      const int sl = c->slot_of[e];
+      if (sl >= 0 && !pl[e]) {
+        (hits[e] > 0 ? free_after_gemm1 : free_now).push_back(sl);
+        c->owner[sl] = -1;
+        c->slot_of[e] = -1;
+      }
+    }
+    // plan copies: hit misses in bucket order (resident-marked -> pool slot, else staging),
+    // then eager promotions without hits
+    struct Copy { int e, dst, off, m; bool after_gemm1, staged; };
+    std::vector<Copy> hit_copies, cold_copies;
+    size_t fn = 0, fa = 0;
+    auto take_slot = [&](bool& after) -> int {
+      if (fn < free_now.size()) { after = false; return free_now[fn++]; }
+      after = true;
+      return free_after_gemm1[fa++];
+    };
+    for (int i = 0; i < hinfo->n_miss; ++i) {
+      const int e = miss_e[i];
+      Copy cp{e, -1, miss_off[i], miss_m[i], false, false};
+      if (pl[e]) {
+        cp.dst = take_slot(cp.after_gemm1);
+        c->owner[cp.dst] = e;
+        c->slot_of[e] = cp.dst;
+      } else {
+        cp.staged = true;
+      }
+      hit_copies.push_back(cp);
+    }
+    if (!lazy) {
+      for (int e = 0; e < E; ++e)
+        if (pl[e] && c->slot_of[e] < 0 && hits[e] == 0) {
+          Copy cp{e, -1, 0, 0, false, false};
+          cp.dst = take_slot(cp.after_gemm1);
+          c->owner[cp.dst] = e;
+          c->slot_of[e] = cp.dst;
+          cold_copies.push_back(cp);
+        }
+    }
+    // order: immediate pool copies and staged ones first, slots freed by GEMM#1 last
+    std::stable_partition(hit_copies.begin(), hit_copies.end(),
+                          [](const Copy& a) { return !a.after_gemm1; });
+    // chunks: <= half staging slots each
+    std::vector<std::pair<int, int>> chunks;  // [begin, end) into hit_copies
+    {
+      int b = 0, used = 0;
+      for (int i = 0; i < (int)hit_copies.size(); ++i) {
+        const bool boundary = (hit_copies[i].staged && used == half) ||
+                              (i > b && hit_copies[i].after_gemm1 && !hit_copies[i - 1].after_gemm1);
+        if (boundary) { chunks.push_back({b, i}); b = i; used = 0; }
+        if (hit_copies[i].staged) used++;
+      }
+      if (b < (int)hit_copies.size()) chunks.push_back({b, (int)hit_copies.size()});
+    }
+    if ((int)chunks.size() > c->max_chunks) return fail(TIDE_EINVAL, "too many staged chunks");
+    // work lists for the staged chunks (uploaded once, before the first chunk FFN)
+    int ne = 0;
+    std::vector<int> chunk_first(chunks.size() + 1, 0);
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+      chunk_first[ci] = ne;
+      int stage_i = 0;
+      for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
+        Copy& cp = hit_copies[i];
+        if (cp.staged) cp.dst = C + (int)(ci % 2) * half + (stage_i++);
+        for (int t = 0; t < cp.m; t += kMaxTok)
+          c->h_entries2[ne++] = make_int4(cp.dst, cp.off + t, std::min(kMaxTok, cp.m - t), 0);
+      }
+      c->h_ctrl2[2 * ci] = ne - chunk_first[ci];
+      c->h_ctrl2[2 * ci + 1] = 0;
+    }
+    chunk_first[chunks.size()] = ne;
+    staged_entries = ne;
+    int* h_done2 = c->h_ctrl2 + 2 * c->max_chunks;
+    for (int i = 0; i < ne; ++i) h_done2[i] = 0;
+    if (!chunks.empty()) {
+      CU_TRY(cudaMemcpyAsync(c->entries2, c->h_entries2, sizeof(int4) * ne, cudaMemcpyHostToDevice, st));
+      CU_TRY(cudaMemcpyAsync(c->ctrl2, c->h_ctrl2, sizeof(int) * 2 * chunks.size(),
+                             cudaMemcpyHostToDevice, st));
+      CU_TRY(cudaMemcpyAsync(c->done2, h_done2, sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+    }
+    // a6: copies on the side stream; a8: FFN per chunk on the main stream
+    bool waited_gemm1 = false;
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+      if (ci >= 2) CU_TRY(cudaStreamWaitEvent(c->side, c->ev_chunk_done[ci - 2], 0));
+      for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
+        const Copy& cp = hit_copies[i];
+        if (cp.after_gemm1 && !waited_gemm1) {
+          CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
+          waited_gemm1 = true;
+        }
+        CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
+                               cudaMemcpyHostToDevice, c->side));
+        copies++;
+      }
+      CU_TRY(cudaEventRecord(c->ev_chunk_ready[ci], c->side));
+      CU_TRY(cudaStreamWaitEvent(st, c->ev_chunk_ready[ci], 0));
+      s = launch_ffn(c, c->entries2 + chunk_first[ci], c->ctrl2 + 2 * ci, c->ctrl2 + 2 * ci + 1,
+                     c->done2 + chunk_first[ci], st);
+      if (s != TIDE_OK) return s;
+      CU_TRY(cudaEventRecord(c->ev_chunk_done[ci], st));
+    }
+    for (const Copy& cp : cold_copies) {
+      if (cp.after_gemm1 && !waited_gemm1) {
+        CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
+        waited_gemm1 = true;
+      }
+      CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
+                             cudaMemcpyHostToDevice, c->side));
+      copies++;
+    }
+    CU_TRY(cudaEventRecord(c->ev_side_done, c->side));
+    CU_TRY(cudaStreamWaitEvent(st, c->ev_side_done, 0));
+    // publish the slot map for the next step's route kernel
+    for (int e = 0; e < E; ++e) c->h_slot_of[e] = c->slot_of[e];
+    CU_TRY(cudaMemcpyAsync(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice, st));
+  }
+
+  // ---------------- a10 combine
+  if (N > 0) {
+    dim3 grid(N, (H + 1023) / 1024);
+    if (c->bf16)
+      tide_combine_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+          c->y_perm, c->gates, c->pos, c->info, static_cast<__nv_bfloat16*>(out), N, k, H,
+          shared ? 1 : 0);
+    else
+      tide_combine_kernel<float><<<grid, 256, 0, st>>>(c->y_perm, c->gates, c->pos, c->info,
+                                                       static_cast<float*>(out), N, k, H,
+                                                       shared ? 1 : 0);
+    CU_TRY(cudaGetLastError());
+  }
+  if (dbg) {
+    if (dbg->topk_idx) CU_TRY(cudaMemcpyAsync(dbg->topk_idx, c->topk, sizeof(int) * N * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->gates) CU_TRY(cudaMemcpyAsync(dbg->gates, c->gates, sizeof(float) * N * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->pos) CU_TRY(cudaMemcpyAsync(dbg->pos, c->pos, sizeof(int) * N * k, cudaMemcpyDeviceToDevice, st));
+    if (dbg->order) CU_TRY(cudaMemcpyAsync(dbg->order, c->order, sizeof(int) * E, cudaMemcpyDeviceToDevice, st));
+    if (dbg->offsets) CU_TRY(cudaMemcpyAsync(dbg->offsets, c->offsets, sizeof(int) * (E + 1), cudaMemcpyDeviceToDevice, st));
+    if (dbg->logits) CU_TRY(cudaMemcpyAsync(dbg->logits, c->logits, sizeof(float) * N * E, cudaMemcpyDeviceToDevice, st));
+  }
+  if (stats) {
+    RouteInfo local;
+    if (!pool_mode) {
+      CU_TRY(cudaMemcpyAsync(&local, c->info, sizeof(RouteInfo), cudaMemcpyDeviceToHost, st));
+      CU_TRY(cudaStreamSynchronize(st));
+      hinfo = &local;
+      if (local.status != 0)
+        return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
+                    step, capacity);
+    } else {
+      CU_TRY(cudaStreamSynchronize(st));
+    }
+    fill_stats(c, hinfo, N, copies, hinfo->n_entries + staged_entries, stats);
+  }
+  return TIDE_OK;
+}
+
+}  // extern "C"

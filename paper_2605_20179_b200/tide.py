@@ -1,0 +1,214 @@
+"""ctypes binding of libtide.so (include/tide.h) -- argument marshalling only.
+
+Every step of the TIDE layer-step runs in the CUDA kernels of libtide.so.  This
+module turns torch tensors into device pointers and the current torch stream
+into a cudaStream_t; it has no compute of its own and no CPU fallback: if the
+shared library is missing or the device is not sm_100, it raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtide.so")
+
+TIDE_OK, TIDE_EINVAL, TIDE_ECAPACITY, TIDE_EPLACEMENT, TIDE_ECUDA, TIDE_ENCCL, TIDE_ENOMEM, \
+    TIDE_EUNSUPPORTED = range(8)
+TIDE_F32, TIDE_BF16 = 0, 1
+TIDE_NORM_TOPK, TIDE_SHARED_EXPERT, TIDE_LAZY_PROMOTE = 1, 2, 4
+
+STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EPLACEMENT",
+                4: "TIDE_ECUDA", 5: "TIDE_ENCCL", 6: "TIDE_ENOMEM", 7: "TIDE_EUNSUPPORTED"}
+
+EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert_elems",
+            "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
+            "tide_moe_step")
+
+
+class TideError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [("num_experts", ctypes.c_int32), ("top_k", ctypes.c_int32),
+                ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("max_tokens", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class ExpertWeights(ctypes.Structure):
+    _fields_ = [("device_all", ctypes.c_void_p), ("host_master", ctypes.c_void_p),
+                ("shared_w", ctypes.c_void_p)]
+
+
+class StepStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "refreshed", "resident_pairs", "nonresident_pairs", "promotions", "evictions",
+        "unique_experts", "experts_streamed", "copies")] + [
+        ("h2d_bytes", ctypes.c_int64), ("weight_bytes_read", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class StepDebug(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("topk_idx", "gates", "pos", "order", "offsets",
+                                                "logits")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libtide.so; raise loudly if it is missing (no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(nvcc, sm_100a); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        L.tide_last_error.restype = ctypes.c_char_p
+        L.tide_expert_elems.restype = ctypes.c_size_t
+        L.tide_expert_bytes.restype = ctypes.c_size_t
+        L.tide_expert_elems.argtypes = [ctypes.POINTER(LayerDesc)]
+        L.tide_expert_bytes.argtypes = [ctypes.POINTER(LayerDesc)]
+        L.tide_ctx_create.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
+        L.tide_ctx_destroy.argtypes = [ctypes.c_void_p]
+        L.tide_ctx_destroy.restype = None
+        L.tide_pack_expert.argtypes = [ctypes.POINTER(LayerDesc)] + [ctypes.c_void_p] * 5
+        L.tide_moe_step.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+            ctypes.POINTER(ExpertWeights), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.POINTER(StepStats), ctypes.POINTER(StepDebug), ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != TIDE_OK:
+        raise TideError(status, lib().tide_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def torch_dtype(code: int):
+    return torch.bfloat16 if code == TIDE_BF16 else torch.float32
+
+
+def make_desc(num_experts, top_k, hidden, ffn, max_tokens, dtype=TIDE_BF16,
+              norm_topk=True, shared_expert=False, lazy_promote=False) -> LayerDesc:
+    flags = (TIDE_NORM_TOPK if norm_topk else 0) | (TIDE_SHARED_EXPERT if shared_expert else 0) \
+        | (TIDE_LAZY_PROMOTE if lazy_promote else 0)
+    return LayerDesc(num_experts, top_k, hidden, ffn, max_tokens, dtype, flags)
+
+
+def expert_elems(desc: LayerDesc) -> int:
+    return lib().tide_expert_elems(ctypes.byref(desc))
+
+
+def expert_bytes(desc: LayerDesc) -> int:
+    return lib().tide_expert_bytes(ctypes.byref(desc))
+
+
+def pack_expert(desc: LayerDesc, w_gate, w_up, w_down, dst, stream=None):
+    """tide_pack_expert: [Wg; Wu; Wd] -> dst (host or device tensors)."""
+    _check(lib().tide_pack_expert(ctypes.byref(desc), _ptr(w_gate), _ptr(w_up), _ptr(w_down),
+                                  _ptr(dst), _stream_ptr(stream)))
+
+
+@dataclass
+class StepOutputs:
+    out: torch.Tensor
+    hit_counts: torch.Tensor
+    placement: torch.Tensor
+    stats: dict | None
+    debug: dict | None
+
+
+class Context:
+    """One tide_ctx (one MoE layer on one device)."""
+
+    def __init__(self, desc: LayerDesc, capacity: int, staging_slots: int = 16, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().tide_ctx_create(ctypes.byref(desc), capacity, staging_slots, device,
+                                     ctypes.byref(h)))
+        self.handle = h
+        self.desc = desc
+        self.capacity = capacity
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib().tide_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def moe_step(self, block_hidden, router_w, *, device_all=None, host_master=None,
+                 shared_w=None, placement, step: int, interval: int, capacity: int | None = None,
+                 out=None, hit_counts=None, placement_out=None, stats: bool = False,
+                 debug: bool = False, stream=None) -> StepOutputs:
+        """tide_moe_step.  Tensors: block_hidden [N,H] (device), router_w [E,H] (device),
+        device_all [E, 3HF] device or host_master [E, 3HF] pinned host, shared_w [3HF]
+        device, placement [E] uint8 device."""
+        d = self.desc
+        N = block_hidden.shape[0]
+        dev = block_hidden.device
+        if out is None:
+            out = torch.empty(N, d.hidden, dtype=block_hidden.dtype, device=dev)
+        if hit_counts is None:
+            hit_counts = torch.empty(d.num_experts, dtype=torch.int32, device=dev)
+        if placement_out is None:
+            placement_out = torch.empty(d.num_experts, dtype=torch.uint8, device=dev)
+        w = ExpertWeights(None if device_all is None else device_all.data_ptr(),
+                          None if host_master is None else host_master.data_ptr(),
+                          None if shared_w is None else shared_w.data_ptr())
+        st = StepStats() if stats else None
+        dbg_t = None
+        dbg = None
+        if debug:
+            k, E = d.top_k, d.num_experts
+            dbg_t = {"topk_idx": torch.empty(N, k, dtype=torch.int32, device=dev),
+                     "gates": torch.empty(N, k, dtype=torch.float32, device=dev),
+                     "pos": torch.empty(N, k, dtype=torch.int32, device=dev),
+                     "order": torch.empty(E, dtype=torch.int32, device=dev),
+                     "offsets": torch.empty(E + 1, dtype=torch.int32, device=dev),
+                     "logits": torch.empty(N, E, dtype=torch.float32, device=dev)}
+            dbg = StepDebug(*(dbg_t[n].data_ptr() for n, _ in StepDebug._fields_))
+        _check(lib().tide_moe_step(
+            self.handle, _ptr(block_hidden), N, _ptr(router_w), ctypes.byref(w), _ptr(placement),
+            step, interval, self.capacity if capacity is None else capacity, _ptr(out),
+            _ptr(hit_counts), _ptr(placement_out), ctypes.byref(st) if st is not None else None,
+            ctypes.byref(dbg) if dbg is not None else None, _stream_ptr(stream)))
+        return StepOutputs(out, hit_counts, placement_out, st.as_dict() if st else None, dbg_t)
+
+
+def pack_layer(desc: LayerDesc, wg, wu, wd, out=None):
+    """Pack E experts ([E,F,H], [E,F,H], [E,H,F] tensors, any device) into
+    [E, 3HF] (allocated on wg's device if ``out`` is None)."""
+    E = wg.shape[0]
+    n = expert_elems(desc)
+    if out is None:
+        out = torch.empty(E, n, dtype=wg.dtype, device=wg.device)
+    for e in range(E):
+        pack_expert(desc, wg[e], wu[e], wd[e], out[e])
+    return out
