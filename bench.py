@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- block-tokens/s per MoE layer-step of the TIDE hot path on B200.
+
+One bench *step* = one denoising step of the block through every MoE layer of
+the stack (20 layers for the mini config); each layer-step is the whole hot
+path (router, top-k, hits, refresh/placement, permutation, grouped SwiGLU FFN
+on tcgen05, combine; pinned-host serving when capacity < E), one
+tide_moe_step call through the C ABI.
+
+  value  = tokens x layer-steps / device time (CUDA events, max over ranks)
+  e2e    = same metric with the block's hidden states H2D-copied from pinned
+           host before, and the output D2H-copied after, every layer-step
+  roofline = the grouped FFN kernel's algorithmic HBM bytes / its measured
+           average launch time vs MEASURED_PEAKS.json hbm_gbs
+
+`--impl reference` times the fp64 CPU oracle (the reference arm of this tier)
+on a bounded sample of the same workload.  Multi-GPU (torchrun): every rank
+runs its own blocks through its own replica of the stack (weak scaling, no
+data-path collective); EP is listed in DESIGN.md as next.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import tidegen as g  # noqa: E402
+
+METRIC = "block-tokens/sec per MoE layer-step"
+UNIT = "block-tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["tide", "reference"], default="tide")
+    ap.add_argument("--config", choices=["mini", "sweep", "flash1"], default="mini")
+    ap.add_argument("--capacity", type=int, default=0, help="0 = all experts in HBM (C = E)")
+    ap.add_argument("--interval", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=0, help="override the stack depth")
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def shape_for(args) -> g.Shape:
+    if args.config == "mini":
+        s = g.MINI
+    elif args.config == "sweep":
+        s = g.SWEEP
+    else:  # one flash-shaped layer stack that fits HBM at C = E
+        s = g.Shape("flash1", 256, 8, 4096, 1024, 8, 32)
+    if args.layers:
+        s = g.Shape(s.name, s.num_experts, s.top_k, s.hidden, s.ffn, args.layers, s.tokens,
+                    s.steps, s.interval, s.capacity, s.dtype, s.shared_expert)
+    return s
+
+
+def workload_str(s: g.Shape, cap: int, interval: int) -> str:
+    return (f"{s.name}: LLaDA2.0-{'mini' if s.hidden == 2048 else 'flash'}-shaped MoE stack, "
+            f"{s.layers} layers, E={s.num_experts} top-{s.top_k}"
+            f"{' + shared expert' if s.shared_expert else ''}, H={s.hidden}, F={s.ffn}, "
+            f"{s.tokens} tokens per layer-step ({s.tokens // 32} block(s) of 32), "
+            f"capacity {cap}{' (all experts in HBM)' if cap == s.num_experts else ' (pinned-host serving)'}, "
+            f"refresh interval {interval}, T={s.steps} steps per block")
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ oracle baseline
+def oracle_rate(shape: g.Shape, seed: int, budget_s: float, tokens: int, wt_host=None):
+    """Time the fp64 CPU oracle (as it stands, single thread) on full layer-steps
+    of `tokens` tokens of layer 0, until `budget_s` seconds are spent."""
+    import oracle
+    if wt_host is None:
+        wr, wg, wu, wd, sh = g.layer_torch(shape, seed, 0, "cpu")
+        to = g.torch_to_np
+        wt_host = oracle.Layer(to(wr), to(wg), to(wu), to(wd),
+                               tuple(to(a) for a in sh) if sh else None)
+    xs = g.block_hidden_np(shape, seed, 0, steps=shape.steps, tokens=tokens)
+    E = shape.num_experts
+    p = np.zeros(E, np.uint8)
+    n_steps, t0 = 0, time.perf_counter()
+    times = []
+    while True:
+        t = n_steps % shape.steps
+        a = time.perf_counter()
+        r = oracle.moe_step(wt_host, xs[t], shape.top_k, p, t, 4, E)
+        times.append(time.perf_counter() - a)
+        p = r.placement
+        n_steps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = sum(times)
+    return {"value": tokens * n_steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n_steps} full layer-steps (router..combine, fp64, single thread) of "
+                      f"layer 0, {tokens} tokens each, steps 0..{n_steps - 1} of the block",
+            "ms_per_layer_step": 1e3 * el / n_steps}, times
+
+
+# ------------------------------------------------------------------ main arm
+def run_tide(args, rank: int, world: int, local_rank: int):
+    from paper_2605_20179_b200 import tide
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    s = shape_for(args)
+    E, k, H, F, N, Lyr = s.num_experts, s.top_k, s.hidden, s.ffn, s.tokens, s.layers
+    cap = args.capacity or E
+    pool_mode = cap < E
+    desc = tide.make_desc(E, k, H, F, N, tide.TIDE_BF16, shared_expert=s.shared_expert)
+    seed = args.seed + 1000 * rank  # each rank runs its own blocks (weak scaling)
+
+    # weights: generated on the device (bit-identical to the host generator), packed by the
+    # product API (tide_pack_expert); one context per layer
+    layers = []
+    for l in range(Lyr):
+        wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev)
+        packed = tide.pack_layer(desc, wg, wu, wd)
+        del wg, wu, wd
+        shared = torch.cat([a.reshape(-1) for a in sh]).contiguous() if sh else None
+        w = {"device_all": packed} if not pool_mode else {"host_master": packed.cpu().pin_memory()}
+        if pool_mode:
+            del packed
+        layers.append(dict(router=wr, w=w, shared=shared,
+                           ctx=tide.Context(desc, cap, 16, local_rank),
+                           x=g.block_hidden_torch(s, seed, l, dev),
+                           pl=torch.zeros(E, dtype=torch.uint8, device=dev),
+                           hits=torch.empty(E, dtype=torch.int32, device=dev),
+                           out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
+    torch.cuda.synchronize()
+    T = s.steps
+
+    def layer_step(L, t, x=None, stats=False):
+        return L["ctx"].moe_step(L["x"][t] if x is None else x, L["router"], **L["w"],
+                                 shared_w=L["shared"], placement=L["pl"], step=t,
+                                 interval=args.interval, out=L["out"], hit_counts=L["hits"],
+                                 placement_out=L["pl"], stats=stats)
+
+    def bench_step(i):
+        t = i % T
+        for L in layers:
+            layer_step(L, t)
+
+    for i in range(args.warmup):
+        bench_step(i)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed_region(phase_timing: bool):
+        for L in layers:
+            L["ctx"].set_timing(phase_timing)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for i in range(args.steps):
+            bench_step(args.warmup + i)
+        e1.record(st)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        if world > 1:
+            tm = torch.tensor([t], device=dev)
+            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+            t = float(tm.item())
+        ph = [L["ctx"].timing() for L in layers] if phase_timing else None
+        for L in layers:
+            L["ctx"].set_timing(False)
+        return t, ph
+
+    # region 1: the headline number (no per-phase events in the stream)
+    clk = Clocks(local_rank)
+    ms, _ = timed_region(False)
+    clocks = clk.stop()
+    # region 2: same steps with per-phase CUDA events on the launching stream (roofline)
+    ms_phased, phases = timed_region(True)
+    layer_steps = args.steps * Lyr
+    value = N * layer_steps * world / (ms / 1e3)
+
+    # algorithmic FFN bytes of exactly the timed (layer, t) sequence: replay with stats
+    # (untimed; routing is deterministic, so the same experts are hit)
+    for L in layers:
+        L["pl"].zero_()
+    for i in range(args.warmup):
+        for L in layers:
+            layer_step(L, i % T)
+    ffn_bytes, uniq, w_read, copies, h2d = 0, 0, 0, 0, 0
+    R = N * k + (N if s.shared_expert else 0)
+    act_bytes = R * (H * 2 + 2 * F * 2 + H * 4)
+    for i in range(args.steps):
+        for L in layers:
+            r = layer_step(L, (args.warmup + i) % T, stats=True)
+            u = r.stats["unique_experts"] + (1 if s.shared_expert else 0)
+            uniq += u
+            w_read += r.stats["weight_bytes_read"]
+            ffn_bytes += u * s.expert_bytes + act_bytes
+            copies += r.stats["copies"]
+            h2d += r.stats["h2d_bytes"]
+    ffn_ms = sum(p["ffn_ms"] for p in phases)
+    ffn_launches = sum(p["ffn_launches"] for p in phases)
+    launches = sum(p["launches"] for p in phases)
+    tot = {kk: sum(p[kk] for p in phases) for kk in ("router_ms", "route_ms", "gather_ms",
+                                                      "ffn_ms", "staged_ms", "combine_ms",
+                                                      "total_ms")}
+    # the resident FFN launch is one per layer-step: its bytes per launch
+    per_launch_bytes = ffn_bytes / layer_steps
+    ffn_avg_s = (tot["ffn_ms"] / 1e3) / layer_steps
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
+        "fallback 6.65 TB/s (B200_PROFILING.md)"
+    achieved = per_launch_bytes / ffn_avg_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ffn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(s.name)
+        except Exception:
+            traffic = None
+    flops_per_layer_step = 2 * N * k * 3 * H * F + (2 * N * 3 * H * F if s.shared_expert else 0)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "tide_ffn_kernel (grouped SwiGLU, tcgen05 + TMA)",
+                "peak_source": peak_src,
+                "bytes_per_launch": round(per_launch_bytes),
+                "avg_launch_us": round(ffn_avg_s * 1e6, 2),
+                "ffn_share_of_step": round(tot["ffn_ms"] / max(tot["total_ms"], 1e-9), 4),
+                "tensor_frac": round(flops_per_layer_step / ffn_avg_s / 1e12 /
+                                     peaks.get("bf16_tflops", 1590.0), 5),
+                "unique_experts_per_layer_step": round(uniq / layer_steps, 2)}
+
+    # e2e: hidden states from pinned host in, output to pinned host out, every layer-step
+    e2e = None
+    if not args.no_e2e:
+        xh = [L["x"].cpu().pin_memory() for L in layers]
+        oh = torch.empty(N, H, dtype=torch.bfloat16).pin_memory()
+        xd = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for i in range(args.steps):
+            t = (args.warmup + i) % T
+            for li, L in enumerate(layers):
+                xd.copy_(xh[li][t], non_blocking=True)
+                layer_step(L, t, x=xd)
+                oh.copy_(L["out"], non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tm = torch.tensor([ems], device=dev)
+            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+            ems = float(tm.item())
+        e2e = {"value": N * layer_steps * world / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": Lyr * N * H * 2, "d2h_bytes_per_step": Lyr * N * H * 2,
+               "ms_per_step": ems / args.steps,
+               "note": "tide_moe_step through the C ABI; per layer-step the block's hidden "
+                       "states are copied from pinned host and the output back"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu, _ = oracle_rate(s, args.seed, args.cpu_seconds, tokens=min(N, 32))
+
+    res = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and "
+                   "calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)",
+           "config": {"workload": workload_str(s, cap, args.interval), "layers": Lyr,
+                      "tokens_per_layer_step": N, "num_experts": E, "top_k": k, "hidden": H,
+                      "ffn": F, "capacity": cap, "interval": args.interval,
+                      "parallelism": f"replicas x{world} (each rank its own blocks)",
+                      "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
+                            "through the stack between reuses"},
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": launches * world if rank == 0 else launches,
+           "clocks": clocks,
+           "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()},
+           "ms_per_step_with_phase_events": round(ms_phased / args.steps, 4),
+           "io": {"copies": copies, "h2d_bytes": h2d} if pool_mode else None}
+    return res
+
+
+def run_reference(args):
+    """Reference arm of this tier: the fp64 CPU oracle, as it stands, timed on the
+    host cores on a bounded sample of the bench workload."""
+    import oracle
+    s = shape_for(args)
+    N = min(s.tokens, 8)
+    wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, 0, "cpu")
+    to = g.torch_to_np
+    L = oracle.Layer(to(wr), to(wg), to(wu), to(wd), tuple(to(a) for a in sh) if sh else None)
+    xs = g.block_hidden_np(s, args.seed, 0, steps=s.steps, tokens=N)
+    E = s.num_experts
+    p = np.zeros(E, np.uint8)
+    for i in range(args.warmup):
+        p = oracle.moe_step(L, xs[i % s.steps], s.top_k, p, i % s.steps, args.interval, E).placement
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        t = (args.warmup + i) % s.steps
+        p = oracle.moe_step(L, xs[t], s.top_k, p, t, args.interval, E).placement
+    el = time.perf_counter() - t0
+    v = N * args.steps / el
+    sample = (f"each step = one full layer-step (router..combine, fp64, single thread) of layer 0 "
+              f"on {N} of the block's {s.tokens} tokens")
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * el / args.steps, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_str(s, E, args.interval) + f" [oracle sample: {N} tokens]"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_tide(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,20 @@ TIDE_API tide_status tide_moe_step(tide_ctx* ctx, const void* block_hidden, int3
                           uint8_t* placement_out, tide_step_stats* stats, tide_step_debug* dbg,
                           void* stream);
 
+/* Per-phase device timing (CUDA events recorded on the step's stream at phase
+ * boundaries).  Enabling resets the accumulators; tide_ctx_get_timing waits
+ * for the recorded events, adds their elapsed times and clears them.
+ *  router/route/gather/ffn/combine: a1, a2-a5, a5 gather, a7+a9 (experts in HBM),
+ *  a10; staged: from the end of the resident FFN to the start of the combine
+ *  in host_master mode (H2D waits + a8 FFN over staged chunks).
+ *  launches: kernels this context launched while timing was enabled.        */
+typedef struct {
+  double router_ms, route_ms, gather_ms, ffn_ms, staged_ms, combine_ms, total_ms;
+  int64_t steps, launches, ffn_launches;
+} tide_phase_times;
+TIDE_API tide_status tide_ctx_set_timing(tide_ctx* ctx, int32_t enable);
+TIDE_API tide_status tide_ctx_get_timing(tide_ctx* ctx, tide_phase_times* out);
+
 /* Thread-local description of the last failure on this thread. */
 TIDE_API const char* tide_last_error(void);
 

@@ -31,27 +31,37 @@ constexpr int kTileM = 128;
 constexpr int kATile = kTileM * 128;           // 16 KB: 128 rows x 128 B (one K block)
 constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 128 B
 constexpr int kStageBytes = 2 * kATile + kBTile;
-constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048;
+constexpr int kMaxEntriesSmem = 1280;          // work entries built per CTA (E + N*k/128 + ...)
+constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem;
 
 struct FfnParams {
   CUtensorMap map_gu;    // routed pool viewed as rows of H elements (gate/up rows)
   CUtensorMap map_d;     // routed pool viewed as rows of F elements (down rows)
   CUtensorMap map_gu_s;  // shared expert, rows of H
   CUtensorMap map_d_s;   // shared expert, rows of F
-  CUtensorMap map_x;     // X_perm [rows, H]
+  CUtensorMap map_x;     // x_in [maxN, H], box = 1 row (tile::gather4)
   CUtensorMap map_h;     // h_perm [rows, F]
-  const int4* entries;   // {slot, row offset, tokens, flags(bit0 = shared)}
+  // work entries {weight slot, first h/y row, m | flags << 16, token-list index};
+  // flags bit0: shared-expert weights, bit1: identity token list (token = index + j).
+  // build mode (cnt != nullptr): every CTA builds the list from the per-expert counts:
+  // experts in id order with m > 0 and (slot_of == nullptr or slot_of[e] >= 0), rows
+  // off[e] = prefix of counts in id order, then the shared expert (rows N*k + n).
+  const int* cnt;        // [E] per-expert token counts (build mode)
+  const int* slot_of;    // [E] pool slot (nullptr: slot = e)
+  int* off_out;          // [E] row offsets written by CTA 0 (build mode; read by combine)
+  const int4* entries;   // global mode: host-built list
   const int* n_entries;
+  const int* list;       // [E * maxN] token lists
   int* sched;
   int* done;
   void* h_out;
   float* y_out;
-  int H, F;
+  int H, F, E, maxN, N, k, shared;
 };
 
 struct FfnItem {
   int kind;  // 0 gate/up, 1 down, -1 end
-  int tile, slot, off, m, flags, entry, pad;
+  int tile, slot, off, m, flags, entry, tokbase;
 };
 
 template <typename T>
@@ -74,6 +84,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   uint64_t* iempty = ifull + kItemSlots;
   FfnItem* items = reinterpret_cast<FfnItem*>(iempty + kItemSlots);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(items + kItemSlots);
+  int* s_tok = reinterpret_cast<int*>(tmem_slot + 4);  // producer: row ids of the current item
+  int4* s_ent = reinterpret_cast<int4*>(s_tok + kMaxTok);  // build mode: this CTA's work list
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = p.H, F = p.F;
@@ -100,10 +112,52 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // the combine grid may start its prologue
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
     // ===================== scheduler + TMA producer =====================
-    const int n_ent = *p.n_entries;
+    pdl_wait();  // routing (counts, token lists, x_in) comes from the preceding grid
+    int n_ent;
+    const int4* ents = p.entries;
+    if (p.cnt) {  // build this CTA's copy of the work list (warp 0, expert ranges per lane)
+      const int E = p.E;
+      const int per = (E + 31) >> 5, e0 = min(E, lane * per), e1 = min(E, e0 + per);
+      int rows = 0, nent = 0;
+      for (int e = e0; e < e1; ++e) {
+        const int m = __ldcg(p.cnt + e);
+        const bool in_hbm = !p.slot_of || __ldcg(p.slot_of + e) >= 0;
+        rows += m;
+        nent += (m > 0 && in_hbm) ? (m + kMaxTok - 1) / kMaxTok : 0;
+      }
+      int rows_x = rows, ent_x = nent;  // inclusive warp scans -> exclusive bases
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, rows_x, o), b = __shfl_up_sync(0xffffffffu, ent_x, o);
+        if (lane >= o) { rows_x += a; ent_x += b; }
+      }
+      int row = rows_x - rows, ei = ent_x - nent;
+      for (int e = e0; e < e1; ++e) {
+        const int m = __ldcg(p.cnt + e);
+        const int slot = p.slot_of ? __ldcg(p.slot_of + e) : e;
+        if (blockIdx.x == 0) p.off_out[e] = row;
+        if (m > 0 && slot >= 0)
+          for (int c = 0; c * kMaxTok < m; ++c)
+            s_ent[ei++] = make_int4(slot, row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
+                                    e * p.maxN + c * kMaxTok);
+        row += m;
+      }
+      n_ent = __shfl_sync(0xffffffffu, ent_x, 31);
+      const int n_sh = p.shared ? (p.N + kMaxTok - 1) / kMaxTok : 0;
+      for (int c = lane; c < n_sh; c += 32)
+        s_ent[n_ent + c] = make_int4(0, p.N * p.k + c * kMaxTok,
+                                     min(kMaxTok, p.N - c * kMaxTok) | (3 << 16), c * kMaxTok);
+      n_ent += n_sh;
+      ents = s_ent;
+      __syncwarp();
+    } else {
+      n_ent = *p.n_entries;
+    }
+    if (lane == 0) {
     const int n1 = n_ent * FT, total = n1 + n_ent * HT;
     const uint64_t pol_w = policy_evict_first(), pol_a = policy_evict_last();
     int stage = 0, islot = 0;
@@ -116,8 +170,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         int entry, tile;
         if (it < n1) { item.kind = 0; entry = it / FT; tile = it % FT; }
         else { item.kind = 1; entry = (it - n1) / HT; tile = (it - n1) % HT; }
-        const int4 en = p.entries[entry];
-        item.tile = tile; item.slot = en.x; item.off = en.y; item.m = en.z; item.flags = en.w;
+        const int4 en = ents[entry];
+        item.tile = tile; item.slot = en.x; item.off = en.y; item.m = en.z & 0xFFFF;
+        item.flags = en.z >> 16; item.tokbase = en.w;
         item.entry = entry;
       }
       mbar_wait(&iempty[islot], iphase ^ 1);
@@ -127,6 +182,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       if (item.kind < 0) break;
       const int nbox = (item.m + 15) >> 4;
       if (item.kind == 0) {
+        // token rows of this entry, gathered straight from x_in (4 rows per gather4;
+        // rows past m repeat the last token -- their MMA columns are discarded)
+        const int ng = (item.m + 3) >> 2;
+        for (int j = 0; j < 4 * ng; ++j) {
+          const int jj = item.tokbase + min(j, item.m - 1);
+          s_tok[j] = (item.flags & 2) ? jj : __ldcg(p.list + jj);
+        }
         const CUtensorMap* ma = (item.flags & 1) ? &p.map_gu_s : &p.map_gu;
         const int rowg = item.slot * 3 * F + item.tile * kTileM;
         const int rowu = rowg + F;
@@ -134,11 +196,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
           mbar_wait(&empty[stage], sphase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + 2 * kATile;
-          mbar_arrive_expect_tx(&full[stage], 2 * kATile + nbox * 2048);
+          mbar_arrive_expect_tx(&full[stage], 2 * kATile + ng * 512);
           tma_load_2d(sa, ma, &full[stage], kb * BK, rowg, pol_w);
           tma_load_2d(sa + kATile, ma, &full[stage], kb * BK, rowu, pol_w);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sb + b * 2048, &p.map_x, &full[stage], kb * BK, item.off + 16 * b, pol_a);
+          for (int gi = 0; gi < ng; ++gi)
+            tma_gather4(sb + gi * 512, &p.map_x, &full[stage], kb * BK,
+                        make_int4(s_tok[4 * gi], s_tok[4 * gi + 1], s_tok[4 * gi + 2], s_tok[4 * gi + 3]),
+                        pol_a);
           if (++stage == kStages) { stage = 0; sphase ^= 1; }
         }
       } else {
@@ -174,6 +238,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         }
       }
     }
+    }  // lane 0
   } else if (warp == 1 && lane == 0) {
     // ===================== MMA issuer (one thread) =====================
     int stage = 0, islot = 0, acc = 0;

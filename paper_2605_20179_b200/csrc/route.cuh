@@ -1,22 +1,32 @@
-// route.cuh -- a1..a5 of the TIDE layer-step:
-//   tide_router_kernel  a1  logits = X Wr^T (fp32 accumulate, blocked order, R-17)
-//   tide_route_kernel   a2  softmax + top-k (lowest id on ties, R-3/R-4)
-//                       a3  hit histogram (shared-memory atomics)
-//                       a4  refresh (step % interval == 0) + top-C placement (R-6/R-8)
-//                       a5  bucket order / offsets / pos (R-11) + FFN work list + miss list
-//   tide_gather_kernel  a5  X_perm[pos[n,j]] = X[n] (and the shared expert's rows)
-//   tide_combine_kernel a10 out[n] = sum_j g[n,j] y[pos[n,j]] (+ y_shared[n]), slot order
+// route.cuh -- a1..a5 and a10 of the TIDE layer-step.
+//
+//   tide_route_kernel  (critical path) one launch, two phases chained by a "last CTA"
+//                      counter per token group:
+//     phase 1 (all CTAs)   a1  logits = X Wr^T for 8 experts x tpc tokens (fp32, blocked
+//                              order, R-17); CTAs of column 0 copy X into x_in (the
+//                              FFN gathers its token rows from there)
+//     phase 2 (last CTA of each token group)
+//                          a2  softmax + top-k (lowest id on ties, R-3/R-4), gates (R-2)
+//                          a3  hits: per-expert token counts + token lists (atomics) and
+//                              per-expert token bitmasks
+//   tide_book_kernel   (off the critical path: concurrent with the FFN)
+//                          a4  refresh (step % interval == 0): top-C placement (R-6/R-8)
+//                          a5  bucket order (resident first, R-11), offsets, pos, info
+//   tide_combine_kernel a10 out[n] = sum_j g[n,j] y[row(n,j)] (+ y_shared[n]), slot order
+//
+// The FFN's rows are grouped by expert in id order (row of pair (n,j) = off[e] +
+// its slot in e's token list); values do not depend on rows, so outputs are bitwise
+// independent of the (atomic) arrival order and of placement.
 #pragma once
 #include "ptx.cuh"
 
 namespace tide {
 
-constexpr int kRouterWarps = 8;    // experts per router CTA
-constexpr int kRouterTokens = 32;  // tokens per router CTA
-constexpr int kRouteThreads = 1024;
-constexpr int kMaxTok = 128;       // tokens per FFN work entry (MMA N <= 128 + gate/up in TMEM)
+constexpr int kRouteThreads = 256;  // 8 warps
+constexpr int kRouterWarps = 8;     // experts per CTA in phase 1 (one per warp)
+constexpr int kMaxTok = 128;        // tokens per FFN work entry (MMA N <= 128)
 
-// ---------------------------------------------------------------- a1 router
+// ---------------------------------------------------------------- a1 helpers
 template <typename T>
 __device__ __forceinline__ float dot16B(uint4 xa, uint4 wa, float acc);
 template <>
@@ -41,39 +51,6 @@ __device__ __forceinline__ float dot16B<float>(uint4 xa, uint4 wa, float acc) {
   return acc;
 }
 
-// grid (ceil(E/8), ceil(N/32)), 256 threads; dynamic smem = 8 * H * sizeof(T).
-// Warp w owns expert e = 8*blockIdx.x + w; its router row is staged in smem once.
-// Lane l accumulates 16-byte chunks l, l+32, ... sequentially in fp32, then a
-// butterfly over the 32 lane partials (every lane ends with identical bits).
-template <typename T>
-__global__ void __launch_bounds__(256) tide_router_kernel(const T* __restrict__ x,
-                                                          const T* __restrict__ wr,
-                                                          float* __restrict__ logits, int N, int E,
-                                                          int H) {
-  extern __shared__ __align__(16) unsigned char router_smem[];
-  uint4* w_s = reinterpret_cast<uint4*>(router_smem);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int e0 = blockIdx.x * kRouterWarps;
-  const int chunks = H * (int)sizeof(T) / 16;
-  const int rows = min(kRouterWarps, E - e0);
-  for (int i = threadIdx.x; i < rows * chunks; i += blockDim.x)
-    w_s[i] = __ldg(reinterpret_cast<const uint4*>(wr + (size_t)e0 * H) + i);
-  __syncthreads();
-  const int e = e0 + warp;
-  if (e >= E) return;
-  const uint4* wrow = w_s + warp * chunks;
-  const int n0 = blockIdx.y * kRouterTokens, n1 = min(N, n0 + kRouterTokens);
-  for (int n = n0; n < n1; ++n) {
-    const uint4* xrow = reinterpret_cast<const uint4*>(x + (size_t)n * H);
-    float acc = 0.f;
-    for (int c = lane; c < chunks; c += 32) acc = dot16B<T>(__ldg(xrow + c), wrow[c], acc);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) logits[(size_t)n * E + e] = acc;
-  }
-}
-
-// ---------------------------------------------------------------- a2..a5 route
 // Info block written for the host (one D2H copy in host_master mode).
 struct RouteInfo {
   int status;          // 0 ok, 3 = TIDE_EPLACEMENT
@@ -81,316 +58,378 @@ struct RouteInfo {
   int n_miss;          // hit experts not loaded in HBM
   int refreshed;
   int promotions, evictions, resident_pairs, unique_experts;
-  int sched;           // FFN work counter (zeroed here)
-  int pad[7];
-  // followed by: miss_e[E], miss_off[E], miss_m[E], hits[E] (int32), placement_out[E] (u8)
+  int pad[8];
+  // followed by: hits[E] (int32), placement_out[E] (u8)
 };
 
 struct RouteParams {
-  const float* logits;
-  const uint8_t* placement_in;
-  const int* slot_of;   // [E] pool slot of each expert, -1 if not in HBM; nullptr: all in HBM (slot = e)
-  int N, E, k, norm_topk, refresh, capacity, shared;
+  const void* x;        // [N,H] caller's block hidden states
+  const void* wr;       // [E,H] router
+  void* x_in;           // [maxN,H] context copy of X (FFN gather source)
+  float* logits;        // [N,E]
+  int N, E, H, k, tpc, norm_topk, maxN;
   int* topk_idx;        // [N,k]
   float* gates;         // [N,k]
-  int* pos;             // [N,k]
-  int* order;           // [E]
-  int* offsets;         // [E+1]
+  int* pair_slot;       // [N,k] slot of pair (n,j) in its expert's token list
+  int* cnt;             // [E] this step's per-expert token counts (zero on entry)
+  int* cnt_next;        // [E] the other parity buffer: zeroed here for the next step
+  int* list;            // [E * maxN] tokens of each expert (arrival order)
+  unsigned* mask;       // [E * NW] token bitmasks (zeroed by tide_book_kernel)
+  int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
+  int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
+  int n_zero;
+};
+
+struct BookParams {
+  const int* cnt;       // [E] hits
+  const unsigned* mask; // [E * NW]
+  unsigned* mask_rw;    // same, zeroed after use
+  const int* topk_idx;  // [N,k]
+  const uint8_t* placement_in;
+  int N, E, k, refresh, capacity;
   int* hit_counts;      // [E] caller buffer
   uint8_t* placement_out;  // [E] caller buffer
-  RouteInfo* info;      // info block (+ trailing arrays)
-  int4* entries;        // FFN work list {slot, row offset, tokens, flags}
-  int* done;            // per-entry phase-1 completion counters (zeroed here)
+  int* order;           // [E]
+  int* offsets;         // [E+1]
+  int* pos;             // [N,k]
+  RouteInfo* info;      // + hits[E] + placement_out[E]
 };
 
 __device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
   return va > vb || (va == vb && ia < ib);
 }
 
-// Block-wide exclusive scan of one int per thread (blockDim == 1024).
-__device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
+// In-place exclusive scan of a[0..n) in shared memory by the whole CTA; returns the total.
+__device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 ints*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(n, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += a[i];
+  int incl = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
-  if (lane == 31) warp_sums[warp] = incl;
+  if (lane == 31) scratch[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    int s = warp_sums[lane];
-    int si = s;
+    const int w = lane < nwarps ? scratch[lane] : 0;
+    int wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, si, o);
-      if (lane >= o) si += t;
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
-    warp_sums[lane] = si - s;  // exclusive warp prefix
-    if (lane == 31) *total = si;
+    scratch[lane] = wi - w;
+    if (lane == 31) scratch[32] = wi;
   }
   __syncthreads();
-  int r = warp_sums[warp] + incl - v;
+  int run = scratch[warp] + incl - s;
+  for (int i = b; i < e; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const int total = scratch[32];
   __syncthreads();
-  return r;
+  return total;
 }
 
-// One CTA of 1024 threads.  E <= 1024, N <= 1024, k <= 32.
-// dynamic smem: hits[E] + bstart[E] + order[E] + pl[E](int) + mask[E * NW] (NW = ceil(N/32))
-__global__ void __launch_bounds__(kRouteThreads, 1) tide_route_kernel(const RouteParams p) {
-  extern __shared__ __align__(16) int route_smem[];
-  const int E = p.E, N = p.N, k = p.k;
-  const int NW = (N + 31) >> 5;
-  int* hits = route_smem;
-  int* bstart = hits + E;
-  int* order = bstart + E;
-  int* pl = order + E;
-  unsigned* mask = reinterpret_cast<unsigned*>(pl + E);
-  __shared__ int warp_sums[32];
-  __shared__ int s_total, s_cnt, s_prom, s_evic;
+// grid (ceil(E/8), ceil(N/tpc)), 256 threads.  EPL = logits per lane in the top-k
+// (power of two >= E/32).
+template <typename T, int EPL>
+__global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_flag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = p.E, N = p.N, H = p.H, k = p.k;
+  const int NW = (N + 31) >> 5;
+  const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
+  pdl_wait();     // X may be written by the previous kernel in the stream
+  pdl_trigger();  // let the FFN grid start its prologue
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int i = tid; i < E; i += blockDim.x) p.cnt_next[i] = 0;
+    for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
+  }
 
-  for (int i = tid; i < E; i += blockDim.x) hits[i] = 0;
-  for (int i = tid; i < E * NW; i += blockDim.x) mask[i] = 0u;
-  if (tid == 0) { s_cnt = 0; s_prom = 0; s_evic = 0; }
-  __syncthreads();
-
-  // ---- a2: per-token top-k by k rounds of a warp argmax (value desc, id asc)
-  const int epl = (E + 31) >> 5;  // logits per lane
-  for (int n = warp; n < N; n += 32) {
-    float v[32];
+  // ================= phase 1: router logits (a1)
+  {
+    constexpr int G = 8;  // 16-byte chunks in flight per lane per group
+    const int e = blockIdx.x * kRouterWarps + warp;
+    const int chunks = H * (int)sizeof(T) / 16;
+    const bool copy_x = blockIdx.x == 0 && warp == 0;
+    if (e < E) {
+      const uint4* wrow = reinterpret_cast<const uint4*>(static_cast<const T*>(p.wr) + (size_t)e * H);
+      for (int n = n0; n < n1; n += 2) {
+        const bool two = n + 1 < n1;
+        const uint4* x0 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)n * H);
+        const uint4* x1 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)(two ? n + 1 : n) * H);
+        uint4* y0 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)n * H);
+        uint4* y1 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)(two ? n + 1 : n) * H);
+        float a0 = 0.f, a1 = 0.f;
+        for (int base = 0; base < chunks; base += 32 * G) {
+          uint4 wv[G], xv0[G], xv1[G];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int e = lane + 32 * i;
-      v[i] = (i < epl && e < E) ? p.logits[(size_t)n * E + e] : -INFINITY;
+          for (int i = 0; i < G; ++i) {
+            const int c = base + lane + 32 * i;
+            if (c < chunks) {
+              wv[i] = __ldg(wrow + c);
+              xv0[i] = __ldg(x0 + c);
+              xv1[i] = __ldg(x1 + c);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < G; ++i) {
+            const int c = base + lane + 32 * i;
+            if (c < chunks) {
+              a0 = dot16B<T>(xv0[i], wv[i], a0);
+              a1 = dot16B<T>(xv1[i], wv[i], a1);
+              if (copy_x) {
+                y0[c] = xv0[i];
+                y1[c] = xv1[i];
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if (lane == 0) {
+          p.logits[(size_t)n * E + e] = a0;
+          if (two) p.logits[(size_t)(n + 1) * E + e] = a1;
+        }
+      }
     }
-    unsigned taken = 0u;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  if (tid == 0) p.g_cnt[blockIdx.y] = 0;
+
+  // ================= phase 2: top-k of this token group (a2) + histogram (a3)
+  // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
+  // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
+  for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
+    float v[EPL];
+    int id[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+      id[i] = e;
+    }
+#pragma unroll
+    for (int a = 0; a < EPL; ++a)
+#pragma unroll
+      for (int b = 0; b + 1 < EPL - a; ++b)
+        if (better(v[b + 1], id[b + 1], v[b], id[b])) {
+          const float tv = v[b]; v[b] = v[b + 1]; v[b + 1] = tv;
+          const int ti = id[b]; id[b] = id[b + 1]; id[b + 1] = ti;
+        }
+    float m = v[0];  // row max
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float z = 0.f;   // full-softmax denominator (norm_topk == 0)
+    if (!p.norm_topk) {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) z += expf(v[i] - m);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    }
     int my_e = 0;
     float my_l = 0.f;
     for (int j = 0; j < k; ++j) {
-      float bv = -INFINITY;
-      int bi = 0x7fffffff;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int e = lane + 32 * i;
-        if (i < epl && e < E && !((taken >> i) & 1u) && better(v[i], e, bv, bi)) {
-          bv = v[i];
-          bi = e;
-        }
-      }
+      float bv = v[0];
+      int bi = id[0];
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
       }
-      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      if ((bi & 31) == lane) {
+#pragma unroll
+        for (int i = 0; i + 1 < EPL; ++i) { v[i] = v[i + 1]; id[i] = id[i + 1]; }
+        v[EPL - 1] = -INFINITY;
+        id[EPL - 1] = 0x7fffffff;
+      }
       if (lane == j) { my_e = bi; my_l = bv; }
     }
-    // gates (R-2): softmax probabilities of the selected experts, renormalised or not
-    const float m = __shfl_sync(0xffffffffu, my_l, 0);  // top-1 logit = max
-    float denom;
+    float denom = z;  // gates (R-2)
     if (p.norm_topk) {
       float t = lane < k ? expf(my_l - m) : 0.f;
 #pragma unroll
       for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       denom = t;
-    } else {
-      float z = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int e = lane + 32 * i;
-        if (i < epl && e < E) z += expf(v[i] - m);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-      denom = z;
     }
     if (lane < k) {
       p.topk_idx[(size_t)n * k + lane] = my_e;
       p.gates[(size_t)n * k + lane] = expf(my_l - m) / denom;
-      atomicAdd(&hits[my_e], 1);                                   // a3
-      atomicOr(&mask[my_e * NW + (n >> 5)], 1u << (n & 31));
+      const int slot = atomicAdd(&p.cnt[my_e], 1);
+      p.list[(size_t)my_e * p.maxN + slot] = n;
+      p.pair_slot[(size_t)n * k + lane] = slot;
+      atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
     }
-  }
-  __syncthreads();
-
-  // ---- a4: refresh -> top-C by (hits desc, id asc); otherwise keep the input placement
-  for (int e = tid; e < E; e += blockDim.x) {
-    int res;
-    const int he = hits[e];
-    if (p.refresh) {
-      int rank = 0;
-      for (int f = 0; f < E; ++f) {
-        const int hf = hits[f];
-        rank += (hf > he) || (hf == he && f < e);
-      }
-      res = rank < p.capacity;
-    } else {
-      res = p.placement_in[e] != 0;
-      if (res) atomicAdd(&s_cnt, 1);
-    }
-    pl[e] = res;
-    const int was = p.placement_in[e] != 0;
-    if (res && !was) atomicAdd(&s_prom, 1);
-    if (was && !res) atomicAdd(&s_evic, 1);
-    p.hit_counts[e] = he;
-  }
-  __syncthreads();
-  int* info_arr = reinterpret_cast<int*>(p.info + 1);
-  int* miss_e = info_arr;
-  int* miss_off = miss_e + E;
-  int* miss_m = miss_off + E;
-  int* info_hits = miss_m + E;
-  uint8_t* info_pl = reinterpret_cast<uint8_t*>(info_hits + E);
-  if (!p.refresh && s_cnt > p.capacity) {  // S:49, S:263 budget safety
-    if (tid == 0) {
-      p.info->status = 3;
-      p.info->n_entries = 0;
-      p.info->n_miss = 0;
-      p.info->sched = 0;
-    }
-    return;
-  }
-
-  // ---- a5: bucket order (resident ascending id, then non-resident ascending id)
-  const int e = tid;
-  const int res = (e < E) ? pl[e] : 0;
-  const int res_before = block_excl_scan(res, warp_sums, &s_total);
-  const int n_res = s_total;
-  if (e < E) {
-    const int b = res ? res_before : n_res + (e - res_before);
-    order[b] = e;
-    p.placement_out[e] = (uint8_t)res;
-    info_pl[e] = (uint8_t)res;
-    info_hits[e] = hits[e];
-  }
-  __syncthreads();
-  // offsets over bucket positions
-  const int be = (tid < E) ? order[tid] : 0;
-  const int m_b = (tid < E) ? hits[be] : 0;
-  const int off_b = block_excl_scan(m_b, warp_sums, &s_total);
-  if (tid < E) {
-    bstart[be] = off_b;
-    p.order[tid] = be;
-    p.offsets[tid] = off_b;
-  }
-  if (tid == 0) p.offsets[E] = N * k;
-  // FFN entries (loaded experts, <= kMaxTok tokens each) and the miss list
-  int slot = be;
-  if (p.slot_of && tid < E) slot = p.slot_of[be];
-  const bool loaded = slot >= 0;
-  const int nent = (tid < E && m_b > 0 && loaded) ? (m_b + kMaxTok - 1) / kMaxTok : 0;
-  const int is_miss = (tid < E && m_b > 0 && !loaded) ? 1 : 0;
-  const int ent_off = block_excl_scan(nent, warp_sums, &s_total);
-  const int n_ent_routed = s_total;
-  const int miss_idx = block_excl_scan(is_miss, warp_sums, &s_total);
-  const int n_miss = s_total;
-  for (int c = 0; c < nent; ++c) {
-    p.entries[ent_off + c] = make_int4(slot, off_b + c * kMaxTok, min(kMaxTok, m_b - c * kMaxTok), 0);
-    p.done[ent_off + c] = 0;
-  }
-  if (is_miss) {
-    miss_e[miss_idx] = be;
-    miss_off[miss_idx] = off_b;
-    miss_m[miss_idx] = m_b;
-  }
-  const int n_sh = p.shared ? (N + kMaxTok - 1) / kMaxTok : 0;
-  if (tid < n_sh) {
-    p.entries[n_ent_routed + tid] =
-        make_int4(0, N * k + tid * kMaxTok, min(kMaxTok, N - tid * kMaxTok), 1);
-    p.done[n_ent_routed + tid] = 0;
-  }
-  // resident pairs / unique experts
-  const int rp = (tid < E && pl[be]) ? m_b : 0;
-  const int uq = (tid < E && m_b > 0) ? 1 : 0;
-  __syncthreads();
-  block_excl_scan(rp, warp_sums, &s_total);
-  const int resident_pairs = s_total;
-  block_excl_scan(uq, warp_sums, &s_total);
-  if (tid == 0) {
-    p.info->status = 0;
-    p.info->n_entries = n_ent_routed + n_sh;
-    p.info->n_miss = n_miss;
-    p.info->refreshed = p.refresh;
-    p.info->promotions = s_prom;
-    p.info->evictions = s_evic;
-    p.info->resident_pairs = resident_pairs;
-    p.info->unique_experts = s_total;
-    p.info->sched = 0;
-  }
-  // pos[n,j] = bucket start of its expert + lower tokens that chose the same expert
-  for (int q = tid; q < N * k; q += blockDim.x) {
-    const int n = q / k;
-    const int ee = p.topk_idx[q];
-    const unsigned* mk = mask + ee * NW;
-    int before = 0;
-    for (int w = 0; w < (n >> 5); ++w) before += __popc(mk[w]);
-    before += __popc(mk[n >> 5] & ((1u << (n & 31)) - 1u));
-    p.pos[q] = bstart[ee] + before;
   }
 }
 
-// ---------------------------------------------------------------- a5 gather
-// grid N, 256 threads: X_perm[pos[n,j]] = X[n]; shared expert rows X_perm[N*k + n] = X[n].
-template <typename T>
-__global__ void __launch_bounds__(256) tide_gather_kernel(const T* __restrict__ x,
-                                                          const int* __restrict__ pos,
-                                                          const RouteInfo* __restrict__ info,
-                                                          T* __restrict__ x_perm, int N, int k,
-                                                          int H, int shared) {
-  if (info->status != 0) return;
-  const int n = blockIdx.x;
-  const int chunks = H * (int)sizeof(T) / 16;
-  const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)n * H);
-  __shared__ int rows[33];
-  if (threadIdx.x < k) rows[threadIdx.x] = pos[(size_t)n * k + threadIdx.x];
-  if (threadIdx.x == 0) rows[k] = N * k + n;
+// One CTA (1024 threads): a4 placement and a5 bookkeeping from the hit counts.
+// dynamic smem: 5 * E ints.
+__global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__ BookParams p) {
+  extern __shared__ int book_smem[];
+  __shared__ int s_scratch[33];
+  __shared__ int s_cnt, s_prom, s_evic, s_rp, s_uq;
+  const int tid = threadIdx.x;
+  const int E = p.E, N = p.N, k = p.k;
+  const int NW = (N + 31) >> 5;
+  int* s_hits = book_smem;
+  int* s_pl = s_hits + E;
+  int* s_order = s_pl + E;
+  int* s_bstart = s_order + E;
+  int* s_tmp = s_bstart + E;
+  if (tid == 0) { s_cnt = 0; s_prom = 0; s_evic = 0; s_rp = 0; s_uq = 0; }
+  for (int e = tid; e < E; e += blockDim.x) s_hits[e] = __ldcg(p.cnt + e);
   __syncthreads();
-  const int nrows = k + (shared ? 1 : 0);
-  for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-    const uint4 v = __ldg(src + c);
-    for (int j = 0; j < nrows; ++j)
-      reinterpret_cast<uint4*>(x_perm + (size_t)rows[j] * H)[c] = v;
+  if (p.refresh) {  // rank(e) = #{f : hits[f] > hits[e] or (== and f < e)}
+    const int S = max(1, (int)blockDim.x / E);   // threads per expert
+    const int seg = (E + S - 1) / S;
+    for (int e = tid; e < E; e += blockDim.x) s_tmp[e] = 0;
+    __syncthreads();
+    for (int idx = tid; idx < E * S; idx += blockDim.x) {
+      const int e = idx % E, sg = idx / E;
+      const int f0 = sg * seg, f1 = min(E, f0 + seg);
+      const int he = s_hits[e];
+      int r = 0;
+#pragma unroll 8
+      for (int f = f0; f < f1; ++f) {
+        const int hf = s_hits[f];
+        r += (hf > he) || (hf == he && f < e);
+      }
+      atomicAdd(&s_tmp[e], r);
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) s_pl[e] = s_tmp[e] < p.capacity;
+  } else {
+    for (int e = tid; e < E; e += blockDim.x) {
+      s_pl[e] = p.placement_in[e] != 0;
+      if (s_pl[e]) atomicAdd(&s_cnt, 1);
+    }
+  }
+  __syncthreads();
+  int* info_hits = reinterpret_cast<int*>(p.info + 1);
+  uint8_t* info_pl = reinterpret_cast<uint8_t*>(info_hits + E);
+  for (int e = tid; e < E; e += blockDim.x) {
+    p.hit_counts[e] = s_hits[e];
+    info_hits[e] = s_hits[e];
+  }
+  if (!p.refresh && s_cnt > p.capacity) {  // S:49, S:263 budget safety
+    for (int i = tid; i < E * NW; i += blockDim.x) p.mask_rw[i] = 0u;
+    if (tid == 0) p.info->status = 3;
+    return;
+  }
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int was = p.placement_in[e] != 0, res = s_pl[e];
+    if (res && !was) atomicAdd(&s_prom, 1);
+    if (was && !res) atomicAdd(&s_evic, 1);
+    if (res) atomicAdd(&s_rp, s_hits[e]);
+    if (s_hits[e] > 0) atomicAdd(&s_uq, 1);
+    p.placement_out[e] = (uint8_t)res;
+    info_pl[e] = (uint8_t)res;
+    s_tmp[e] = res;
+  }
+  __syncthreads();
+  // bucket order: resident ascending id, then non-resident ascending id (R-11)
+  const int n_res = block_scan_excl(s_tmp, E, s_scratch);
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int rb = s_tmp[e];
+    s_order[s_pl[e] ? rb : n_res + (e - rb)] = e;
+  }
+  __syncthreads();
+  for (int i = tid; i < E; i += blockDim.x) s_tmp[i] = s_hits[s_order[i]];
+  __syncthreads();
+  block_scan_excl(s_tmp, E, s_scratch);  // offsets over bucket positions
+  for (int i = tid; i < E; i += blockDim.x) {
+    s_bstart[s_order[i]] = s_tmp[i];
+    p.order[i] = s_order[i];
+    p.offsets[i] = s_tmp[i];
+  }
+  if (tid == 0) p.offsets[E] = N * k;
+  __syncthreads();
+  // pos[n,j] = bucket start of its expert + lower tokens that chose the same expert
+  for (int q = tid; q < N * k; q += blockDim.x) {
+    const int n = q / k;
+    const int e = __ldcg(p.topk_idx + q);
+    const unsigned* mk = p.mask + e * NW;
+    int before = 0;
+    for (int w = 0; w < (n >> 5); ++w) before += __popc(__ldcg(mk + w));
+    before += __popc(__ldcg(mk + (n >> 5)) & ((1u << (n & 31)) - 1u));
+    p.pos[q] = s_bstart[e] + before;
+  }
+  __syncthreads();
+  for (int i = tid; i < E * NW; i += blockDim.x) p.mask_rw[i] = 0u;
+  if (tid == 0) {
+    p.info->status = 0;
+    p.info->refreshed = p.refresh;
+    p.info->promotions = s_prom;
+    p.info->evictions = s_evic;
+    p.info->resident_pairs = s_rp;
+    p.info->unique_experts = s_uq;
   }
 }
 
 // ---------------------------------------------------------------- a10 combine
-// grid (N, ceil(H / 1024)), 256 threads x 4 columns.  fp32 FMA over j in slot order
-// (then the shared expert), one rounding to the output dtype (R-14).
+// grid (N, ceil(H / 512)), 128 threads x 4 columns.  row(n,j) = off[e] + slot(n,j).
+// fp32 FMA over j in slot order (then the shared expert), one rounding (R-14).
 template <typename T>
-__global__ void __launch_bounds__(256) tide_combine_kernel(const float* __restrict__ y,
+__global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restrict__ y,
                                                            const float* __restrict__ gates,
-                                                           const int* __restrict__ pos,
-                                                           const RouteInfo* __restrict__ info,
-                                                           T* __restrict__ out, int N, int k, int H,
-                                                           int shared) {
-  if (info->status != 0) return;
+                                                           const int* __restrict__ topk,
+                                                           const int* __restrict__ pair_slot,
+                                                           const int* __restrict__ off,
+                                                           T* __restrict__ out, int N, int k,
+                                                           int H, int shared) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
   if (c >= H) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int j = 0; j < k; ++j) {
-    const float g = __ldg(gates + (size_t)n * k + j);
-    const int r = __ldg(pos + (size_t)n * k + j);
-    const float4 v = __ldg(reinterpret_cast<const float4*>(y + (size_t)r * H + c));
+    const int q = n * k + j;
+    const float g = __ldcg(gates + q);
+    const int r = __ldcg(off + __ldcg(topk + q)) + __ldcg(pair_slot + q);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)r * H + c));
     acc.x = fmaf(g, v.x, acc.x);
     acc.y = fmaf(g, v.y, acc.y);
     acc.z = fmaf(g, v.z, acc.z);
     acc.w = fmaf(g, v.w, acc.w);
   }
   if (shared) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(y + (size_t)(N * k + n) * H + c));
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(N * k + n) * H + c));
     acc.x += v.x;
     acc.y += v.y;
     acc.z += v.z;
     acc.w += v.w;
   }
   T* o = out + (size_t)n * H + c;
-  o[0] = from_f32<T>(acc.x);
-  o[1] = from_f32<T>(acc.y);
-  o[2] = from_f32<T>(acc.z);
-  o[3] = from_f32<T>(acc.w);
+  if constexpr (sizeof(T) == 2) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(o) = pk;
+  } else {
+    *reinterpret_cast<float4*>(o) = acc;
+  }
 }
 
 }  // namespace tide

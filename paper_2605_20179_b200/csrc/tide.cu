@@ -1,11 +1,19 @@
 // tide.cu -- host runtime + C ABI (include/tide.h) of the TIDE MoE layer-step.
 //
 // One tide_ctx per (layer, device).  It owns the workspaces, the HBM slot pool
-// (capacity experts) and staging ring for host_master mode, the side stream used
-// for H2D expert copies, events, and cached TMA tensor maps.  The host side of
-// a step is: validate -> router -> route -> gather -> FFN over experts already
-// in HBM -> [host_master: read the miss list, enqueue H2D copies on the side
-// stream, FFN over each staged chunk once its copy event fires] -> combine.
+// (capacity experts) and staging ring for host_master mode, a side stream, events
+// and cached TMA tensor maps.  A step is, on the caller's stream:
+//
+//   tide_route_kernel    a1 router, a2 top-k/gates, a3 hits + per-expert token lists
+//   tide_ffn_kernel      a7/a9 grouped SwiGLU over the hit experts already in HBM (+ shared)
+//   [host_master only: read the bookkeeping info, enqueue H2D copies of the missing
+//    experts on the side stream (a6), tide_ffn_kernel per staged chunk once its copy
+//    event fires (a8)]
+//   tide_combine_kernel  a10
+//
+// and, concurrently on the side stream (device_all) or before the FFN (host_master),
+//   tide_book_kernel     a4 refresh/placement, a5 bucket order/offsets/pos, info block.
+// Consecutive kernels on the caller's stream use programmatic dependent launch.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -14,6 +22,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/tide.h"
@@ -88,24 +97,30 @@ tide_status make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t cols,
 struct tide_ctx {
   tide_layer_desc d;
   int capacity = 0, staging = 0, device = 0, num_sms = 148;
-  int E = 0, k = 0, H = 0, F = 0, maxN = 0;
+  int E = 0, k = 0, H = 0, F = 0, maxN = 0, NWmax = 1;
   bool bf16 = true;
   size_t eb = 2, expert_elems = 0, expert_bytes = 0;
   int max_rows = 0, max_entries = 0;
+  int parity = 0;  // which of the two count buffers this step uses
 
   // workspaces (device)
   float* logits = nullptr;
   int* topk = nullptr;
   float* gates = nullptr;
+  int* pair_slot = nullptr;
+  int* cnt = nullptr;        // [2][E] per-expert token counts (double-buffered by step parity)
+  int* list = nullptr;       // [E * maxN] per-expert token lists
+  unsigned* mask = nullptr;  // [E * NWmax] per-expert token bitmasks
+  int* g_cnt = nullptr;      // [maxN + 2] route-kernel last-CTA counters
+  int* off = nullptr;        // [E] FFN row offset of each expert (id order)
   int* pos = nullptr;
   int* order = nullptr;
   int* offsets = nullptr;
-  void* x_perm = nullptr;
-  void* h_perm = nullptr;
-  float* y_perm = nullptr;
-  int4* entries = nullptr;
-  int* done = nullptr;
-  RouteInfo* info = nullptr;  // + 4E ints + E bytes
+  void* x_in = nullptr;      // [maxN, H] copy of the block's hidden states (gather4 source)
+  void* h_perm = nullptr;    // [max_rows, F]
+  float* y_perm = nullptr;   // [max_rows, H]
+  int* ffn_ctrl = nullptr;   // [1 + max_entries]: scheduler counter + per-entry done counters
+  RouteInfo* info = nullptr; // + hits[E] + placement[E]
   size_t info_bytes = 0;
   int* slot_of_dev = nullptr;
 
@@ -115,14 +130,15 @@ struct tide_ctx {
   int* ctrl2 = nullptr;            // per chunk {n_entries, sched}
   int* done2 = nullptr;
   int max_chunks = 0, max_entries2 = 0;
-  void* h_info = nullptr;          // pinned mirror of info block
+  void* h_info = nullptr;          // pinned mirror of the info block
   int4* h_entries2 = nullptr;      // pinned
   int* h_ctrl2 = nullptr;          // pinned (ctrl2 + done2 zeros)
   int* h_slot_of = nullptr;        // pinned mirror of slot_of_dev
   std::vector<int> slot_of;        // expert -> pool slot (authoritative)
   std::vector<int> owner;          // pool slot -> expert (-1 free)
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_info = nullptr, ev_gemm1 = nullptr, ev_side_done = nullptr;
+  cudaEvent_t ev_route = nullptr, ev_book = nullptr, ev_info = nullptr, ev_gemm1 = nullptr,
+              ev_side_done = nullptr;
   std::vector<cudaEvent_t> ev_chunk_ready, ev_chunk_done;
 
   // cached tensor maps
@@ -131,7 +147,49 @@ struct tide_ctx {
   int map_src_rows = 0;
   const void* map_shared_src = nullptr;
   bool have_shared_map = false;
+
+  // per-phase timing (tide_ctx_set_timing)
+  bool timing = false;
+  struct Rec { cudaEvent_t ev[7]; int64_t launches, ffn_launches; };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<Rec> pending;
+  tide_phase_times acc{};
+  int64_t launches = 0, ffn_launches = 0;  // kernels launched by this context (lifetime)
 };
+
+static cudaEvent_t take_event(tide_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+static int route_epl(int E) {
+  const int need = (E + 31) / 32;
+  int epl = 1;
+  while (epl < need) epl <<= 1;
+  return epl;
+}
 
 extern "C" {
 
@@ -172,6 +230,11 @@ static tide_status validate_desc(const tide_layer_desc* d) {
     return fail(TIDE_EUNSUPPORTED, "max_tokens %d outside [1, 1024]", d->max_tokens);
   if (d->dtype != TIDE_BF16 && d->dtype != TIDE_F32)
     return fail(TIDE_EUNSUPPORTED, "dtype %d", (int)d->dtype);
+  const int max_ent = d->num_experts + d->max_tokens * d->top_k / kMaxTok + 2 +
+                      (d->max_tokens + kMaxTok - 1) / kMaxTok;
+  if (max_ent > kMaxEntriesSmem)
+    return fail(TIDE_EUNSUPPORTED, "E + N*k/128 too large for the FFN work list (%d > %d)",
+                max_ent, kMaxEntriesSmem);
   return TIDE_OK;
 }
 
@@ -179,9 +242,10 @@ void tide_ctx_destroy(tide_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->side) cudaStreamSynchronize(c->side);
-  void* dev[] = {c->logits, c->topk,  c->gates,    c->pos,   c->order, c->offsets,
-                 c->x_perm, c->h_perm, c->y_perm,  c->entries, c->done, c->info,
-                 c->slot_of_dev, c->pool, c->entries2, c->ctrl2, c->done2};
+  void* dev[] = {c->logits, c->topk,     c->gates,   c->pair_slot, c->cnt,    c->list,
+                 c->mask,   c->g_cnt,    c->off,     c->pos,       c->order,  c->offsets,
+                 c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
+                 c->pool,   c->entries2, c->ctrl2,   c->done2};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -189,9 +253,12 @@ void tide_ctx_destroy(tide_ctx* c) {
     if (p) cudaFreeHost(p);
   for (cudaEvent_t e : c->ev_chunk_ready) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_chunk_done) cudaEventDestroy(e);
-  if (c->ev_info) cudaEventDestroy(c->ev_info);
-  if (c->ev_gemm1) cudaEventDestroy(c->ev_gemm1);
-  if (c->ev_side_done) cudaEventDestroy(c->ev_side_done);
+  for (auto& r : c->pending)
+    for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  cudaEvent_t evs[] = {c->ev_route, c->ev_book, c->ev_info, c->ev_gemm1, c->ev_side_done};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;
 }
@@ -220,7 +287,8 @@ tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t 
   CU_TRY(cudaSetDevice(device));
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
-  if (major != 10) return fail(TIDE_EUNSUPPORTED, "device %d is sm_%d0, this build is sm_100a", device, major);
+  if (major != 10)
+    return fail(TIDE_EUNSUPPORTED, "device %d is sm_%d0, this build is sm_100a", device, major);
 
   tide_ctx* c = new tide_ctx();
   c->d = *d;
@@ -233,6 +301,7 @@ tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t 
   c->H = d->hidden;
   c->F = d->ffn;
   c->maxN = d->max_tokens;
+  c->NWmax = (c->maxN + 31) / 32;
   c->bf16 = d->dtype == TIDE_BF16;
   c->eb = c->bf16 ? 2 : 4;
   c->expert_elems = tide_expert_elems(d);
@@ -244,46 +313,45 @@ tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t 
   ALLOC(c->logits, sizeof(float) * N * E);
   ALLOC(c->topk, sizeof(int) * N * k);
   ALLOC(c->gates, sizeof(float) * N * k);
+  ALLOC(c->pair_slot, sizeof(int) * N * k);
+  ALLOC(c->cnt, sizeof(int) * 2 * E);
+  ALLOC(c->list, sizeof(int) * (size_t)E * N);
+  ALLOC(c->mask, sizeof(unsigned) * E * c->NWmax);
+  ALLOC(c->g_cnt, sizeof(int) * (N + 2));
+  ALLOC(c->off, sizeof(int) * E);
   ALLOC(c->pos, sizeof(int) * N * k);
   ALLOC(c->order, sizeof(int) * E);
   ALLOC(c->offsets, sizeof(int) * (E + 1));
-  ALLOC(c->x_perm, c->eb * (size_t)c->max_rows * c->H);
+  ALLOC(c->x_in, c->eb * (size_t)N * c->H);
   ALLOC(c->h_perm, c->eb * (size_t)c->max_rows * c->F);
   ALLOC(c->y_perm, sizeof(float) * (size_t)c->max_rows * c->H);
-  ALLOC(c->entries, sizeof(int4) * c->max_entries);
-  ALLOC(c->done, sizeof(int) * c->max_entries);
-  c->info_bytes = sizeof(RouteInfo) + sizeof(int) * 4 * E + E;
+  ALLOC(c->ffn_ctrl, sizeof(int) * (1 + c->max_entries));
+  c->info_bytes = sizeof(RouteInfo) + sizeof(int) * E + E;
   ALLOC(c->info, c->info_bytes);
   ALLOC(c->slot_of_dev, sizeof(int) * E);
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_route, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_book, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_info, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_gemm1, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess) {
     tide_ctx_destroy(c);
     return fail(TIDE_ECUDA, "stream/event creation failed");
   }
-  if (make_map(&c->map_x, c->x_perm, c->bf16, c->H, c->max_rows, 16) != TIDE_OK ||
+  if (make_map(&c->map_x, c->x_in, c->bf16, c->H, N, 1) != TIDE_OK ||
       make_map(&c->map_h, c->h_perm, c->bf16, c->F, c->max_rows, 16) != TIDE_OK) {
     std::string m = g_err;
     tide_ctx_destroy(c);
     return fail(TIDE_ECUDA, "%s", m.c_str());
   }
-  // kernel attributes (idempotent)
-  const size_t router_smem = (size_t)kRouterWarps * c->H * c->eb;
-  if (c->bf16) {
-    cudaFuncSetAttribute(tide_router_kernel<__nv_bfloat16>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)router_smem);
+  if (c->bf16)
     cudaFuncSetAttribute(tide_ffn_kernel<__nv_bfloat16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kFfnSmemBytes);
-  } else {
-    cudaFuncSetAttribute(tide_router_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)router_smem);
+  else
     cudaFuncSetAttribute(tide_ffn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kFfnSmemBytes);
-  }
-  const size_t route_smem = sizeof(int) * (4 * E + E * ((N + 31) / 32));
-  cudaFuncSetAttribute(tide_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)route_smem);
+  cudaFuncSetAttribute(tide_book_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(int) * 5 * E));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     tide_ctx_destroy(c);
@@ -326,8 +394,11 @@ static tide_status ensure_pool(tide_ctx* c) {
   return TIDE_OK;
 }
 
-static tide_status launch_ffn(tide_ctx* c, const int4* entries, const int* n_entries, int* sched,
-                              int* done, cudaStream_t st) {
+// build mode: cnt != nullptr (every CTA derives the work list from the counts);
+// global mode: entries/n_entries (host-built staged chunk).
+static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
+                              const int4* entries, const int* n_entries, int* sched, int* done,
+                              int N, cudaStream_t st) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -335,19 +406,31 @@ static tide_status launch_ffn(tide_ctx* c, const int4* entries, const int* n_ent
   p.map_d_s = c->have_shared_map ? c->map_d_s : c->map_d;
   p.map_x = c->map_x;
   p.map_h = c->map_h;
+  p.cnt = cnt;
+  p.slot_of = slot_of;
+  p.off_out = c->off;
   p.entries = entries;
   p.n_entries = n_entries;
+  p.list = c->list;
   p.sched = sched;
   p.done = done;
   p.h_out = c->h_perm;
   p.y_out = c->y_perm;
   p.H = c->H;
   p.F = c->F;
+  p.E = c->E;
+  p.maxN = c->maxN;
+  p.N = N;
+  p.k = c->k;
+  p.shared = (c->d.flags & TIDE_SHARED_EXPERT) ? 1 : 0;
   if (c->bf16)
-    tide_ffn_kernel<__nv_bfloat16><<<c->num_sms, kFfnThreads, kFfnSmemBytes, st>>>(p);
+    CU_TRY(launch_pdl(tide_ffn_kernel<__nv_bfloat16>, dim3(c->num_sms), dim3(kFfnThreads),
+                      kFfnSmemBytes, st, p));
   else
-    tide_ffn_kernel<float><<<c->num_sms, kFfnThreads, kFfnSmemBytes, st>>>(p);
-  CU_TRY(cudaGetLastError());
+    CU_TRY(launch_pdl(tide_ffn_kernel<float>, dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes,
+                      st, p));
+  c->launches++;
+  c->ffn_launches++;
   return TIDE_OK;
 }
 
@@ -372,18 +455,186 @@ static tide_status ensure_weight_maps(tide_ctx* c, const void* src, int rows_exp
   return TIDE_OK;
 }
 
-static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int copies, int entries_total,
-                       tide_step_stats* st) {
+static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, int copies,
+                       int64_t weight_bytes, tide_step_stats* st) {
   st->refreshed = info->refreshed;
   st->resident_pairs = info->resident_pairs;
   st->nonresident_pairs = N * c->k - info->resident_pairs;
   st->promotions = info->promotions;
   st->evictions = info->evictions;
   st->unique_experts = info->unique_experts;
-  st->experts_streamed = info->n_miss;
+  st->experts_streamed = streamed;
   st->copies = copies;
   st->h2d_bytes = (int64_t)copies * (int64_t)c->expert_bytes;
-  st->weight_bytes_read = (int64_t)entries_total * (int64_t)c->expert_bytes;
+  st->weight_bytes_read = weight_bytes;
+}
+
+static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
+                               int refresh, int capacity, int32_t* hit_counts,
+                               uint8_t* placement_out, cudaStream_t st) {
+  BookParams b;
+  b.cnt = cnt;
+  b.mask = c->mask;
+  b.mask_rw = c->mask;
+  b.topk_idx = c->topk;
+  b.placement_in = placement;
+  b.N = N;
+  b.E = c->E;
+  b.k = c->k;
+  b.refresh = refresh;
+  b.capacity = capacity;
+  b.hit_counts = hit_counts;
+  b.placement_out = placement_out;
+  b.order = c->order;
+  b.offsets = c->offsets;
+  b.pos = c->pos;
+  b.info = c->info;
+  tide_book_kernel<<<1, 1024, sizeof(int) * 5 * c->E, st>>>(b);
+  CU_TRY(cudaGetLastError());
+  c->launches++;
+  return TIDE_OK;
+}
+
+// host_master: plan and enqueue the H2D copies (a6) and the staged FFN chunks (a8).
+// Slot semantics (R-12/R-13): an expert in HBM at step start is served from HBM this
+// step; a slot released by an expert that is hit this step is rewritten only after the
+// resident FFN has read it; hit experts not in HBM are copied into a pool slot when in
+// placement', else into the staging ring (not retained); eager promotions copy promoted
+// experts without hits after the hit ones.
+static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const RouteInfo* hinfo,
+                             int N, cudaStream_t st, int* streamed, int* copies,
+                             int64_t* weight_bytes) {
+  const int E = c->E;
+  const int* hits = reinterpret_cast<const int*>(hinfo + 1);
+  const uint8_t* pl = reinterpret_cast<const uint8_t*>(hits + E);
+  const bool lazy = (c->d.flags & TIDE_LAZY_PROMOTE) != 0;
+  const int C = c->capacity, S = c->staging, half = std::max(1, S / 2);
+  const uint8_t* master = static_cast<const uint8_t*>(w->host_master);
+  uint8_t* pool = static_cast<uint8_t*>(c->pool);
+  const size_t xb = c->expert_bytes;
+  std::vector<int> off(E), loaded0(E);
+  for (int e = 0, r = 0; e < E; ++e) {  // same row rule as the FFN's build mode
+    off[e] = r;
+    r += hits[e];
+    loaded0[e] = c->slot_of[e] >= 0;
+    if (hits[e] > 0 && loaded0[e]) *weight_bytes += (int64_t)xb * ((hits[e] + kMaxTok - 1) / kMaxTok);
+  }
+  std::vector<int> free_now, free_after_gemm1;
+  for (int sl = 0; sl < C; ++sl)
+    if (c->owner[sl] < 0) free_now.push_back(sl);
+  for (int e = 0; e < E; ++e) {
+    const int sl = c->slot_of[e];
+    if (sl >= 0 && !pl[e]) {
+      (hits[e] > 0 ? free_after_gemm1 : free_now).push_back(sl);
+      c->owner[sl] = -1;
+      c->slot_of[e] = -1;
+    }
+  }
+  struct Copy { int e, dst; bool after_gemm1, staged; };
+  std::vector<Copy> hit_copies, cold_copies;
+  size_t fn = 0, fa = 0;
+  auto take_slot = [&](bool& after) -> int {
+    if (fn < free_now.size()) { after = false; return free_now[fn++]; }
+    after = true;
+    return free_after_gemm1[fa++];
+  };
+  for (int e = 0; e < E; ++e) {
+    if (hits[e] == 0 || loaded0[e]) continue;
+    Copy cp{e, -1, false, false};
+    if (pl[e]) {
+      cp.dst = take_slot(cp.after_gemm1);
+      c->owner[cp.dst] = e;
+      c->slot_of[e] = cp.dst;
+    } else {
+      cp.staged = true;
+    }
+    hit_copies.push_back(cp);
+  }
+  if (!lazy)
+    for (int e = 0; e < E; ++e)
+      if (pl[e] && c->slot_of[e] < 0 && hits[e] == 0) {
+        Copy cp{e, -1, false, false};
+        cp.dst = take_slot(cp.after_gemm1);
+        c->owner[cp.dst] = e;
+        c->slot_of[e] = cp.dst;
+        cold_copies.push_back(cp);
+      }
+  *streamed = (int)hit_copies.size();
+  std::stable_partition(hit_copies.begin(), hit_copies.end(),
+                        [](const Copy& a) { return !a.after_gemm1; });
+  std::vector<std::pair<int, int>> chunks;  // [begin, end) into hit_copies
+  {
+    int b = 0, used = 0;
+    for (int i = 0; i < (int)hit_copies.size(); ++i) {
+      const bool boundary = (hit_copies[i].staged && used == half) ||
+                            (i > b && hit_copies[i].after_gemm1 && !hit_copies[i - 1].after_gemm1);
+      if (boundary) { chunks.push_back({b, i}); b = i; used = 0; }
+      if (hit_copies[i].staged) used++;
+    }
+    if (b < (int)hit_copies.size()) chunks.push_back({b, (int)hit_copies.size()});
+  }
+  if ((int)chunks.size() > c->max_chunks) return fail(TIDE_EINVAL, "too many staged chunks");
+  int ne = 0;
+  std::vector<int> chunk_first(chunks.size() + 1, 0);
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    chunk_first[ci] = ne;
+    int stage_i = 0;
+    for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
+      Copy& cp = hit_copies[i];
+      if (cp.staged) cp.dst = C + (int)(ci % 2) * half + (stage_i++);
+      const int m = hits[cp.e];
+      for (int t = 0; t < m; t += kMaxTok) {
+        c->h_entries2[ne++] = make_int4(cp.dst, off[cp.e] + t, std::min(kMaxTok, m - t),
+                                        cp.e * c->maxN + t);
+        *weight_bytes += (int64_t)xb;
+      }
+    }
+    c->h_ctrl2[2 * ci] = ne - chunk_first[ci];
+    c->h_ctrl2[2 * ci + 1] = 0;
+  }
+  chunk_first[chunks.size()] = ne;
+  int* h_done2 = c->h_ctrl2 + 2 * c->max_chunks;
+  for (int i = 0; i < ne; ++i) h_done2[i] = 0;
+  if (!chunks.empty()) {
+    CU_TRY(cudaMemcpyAsync(c->entries2, c->h_entries2, sizeof(int4) * ne, cudaMemcpyHostToDevice, st));
+    CU_TRY(cudaMemcpyAsync(c->ctrl2, c->h_ctrl2, sizeof(int) * 2 * chunks.size(),
+                           cudaMemcpyHostToDevice, st));
+    CU_TRY(cudaMemcpyAsync(c->done2, h_done2, sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+  }
+  bool waited_gemm1 = false;
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    if (ci >= 2) CU_TRY(cudaStreamWaitEvent(c->side, c->ev_chunk_done[ci - 2], 0));
+    for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
+      const Copy& cp = hit_copies[i];
+      if (cp.after_gemm1 && !waited_gemm1) {
+        CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
+        waited_gemm1 = true;
+      }
+      CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
+                             cudaMemcpyHostToDevice, c->side));
+      (*copies)++;
+    }
+    CU_TRY(cudaEventRecord(c->ev_chunk_ready[ci], c->side));
+    CU_TRY(cudaStreamWaitEvent(st, c->ev_chunk_ready[ci], 0));
+    tide_status s = launch_ffn(c, nullptr, nullptr, c->entries2 + chunk_first[ci], c->ctrl2 + 2 * ci,
+                               c->ctrl2 + 2 * ci + 1, c->done2 + chunk_first[ci], N, st);
+    if (s != TIDE_OK) return s;
+    CU_TRY(cudaEventRecord(c->ev_chunk_done[ci], st));
+  }
+  for (const Copy& cp : cold_copies) {
+    if (cp.after_gemm1 && !waited_gemm1) {
+      CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
+      waited_gemm1 = true;
+    }
+    CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
+                           cudaMemcpyHostToDevice, c->side));
+    (*copies)++;
+  }
+  CU_TRY(cudaEventRecord(c->ev_side_done, c->side));
+  CU_TRY(cudaStreamWaitEvent(st, c->ev_side_done, 0));
+  for (int e = 0; e < E; ++e) c->h_slot_of[e] = c->slot_of[e];
+  CU_TRY(cudaMemcpyAsync(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice, st));
+  return TIDE_OK;
 }
 
 tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
@@ -424,220 +675,127 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
                                      pool_mode ? c->capacity + c->staging : E,
                                      shared ? w->shared_w : nullptr);
   if (s != TIDE_OK) return s;
+  int* cnt = c->cnt + c->parity * E;
+  int* cnt_next = c->cnt + (c->parity ^ 1) * E;
+  c->parity ^= 1;
 
-  // ---------------- a1 router
-  if (N > 0) {
-    dim3 grid((E + kRouterWarps - 1) / kRouterWarps, (N + kRouterTokens - 1) / kRouterTokens);
-    const size_t sm = (size_t)kRouterWarps * H * c->eb;
-    if (c->bf16)
-      tide_router_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
-          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wr), c->logits,
-          N, E, H);
-    else
-      tide_router_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(x),
-                                                       static_cast<const float*>(wr), c->logits,
-                                                       N, E, H);
-    CU_TRY(cudaGetLastError());
+  tide_ctx::Rec rec{};
+  const int64_t launches0 = c->launches, ffn0 = c->ffn_launches;
+  if (c->timing) {
+    for (cudaEvent_t& e : rec.ev) e = take_event(c);
+    CU_TRY(cudaEventRecord(rec.ev[0], st));
   }
-  // ---------------- a2..a5 route
+  // ---------------- a1..a3: router, top-k, hits and per-expert token lists
   RouteParams rp;
+  rp.x = x;
+  rp.wr = wr;
+  rp.x_in = c->x_in;
   rp.logits = c->logits;
-  rp.placement_in = placement;
-  rp.slot_of = pool_mode ? c->slot_of_dev : nullptr;
   rp.N = N;
   rp.E = E;
+  rp.H = H;
   rp.k = k;
+  rp.tpc = N <= 64 ? 4 : 8;
   rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
-  rp.refresh = refresh;
-  rp.capacity = capacity;
-  rp.shared = shared ? 1 : 0;
+  rp.maxN = c->maxN;
   rp.topk_idx = c->topk;
   rp.gates = c->gates;
-  rp.pos = c->pos;
-  rp.order = c->order;
-  rp.offsets = c->offsets;
-  rp.hit_counts = hit_counts;
-  rp.placement_out = placement_out;
-  rp.info = c->info;
-  rp.entries = c->entries;
-  rp.done = c->done;
-  const size_t route_smem = sizeof(int) * (4 * E + E * ((N + 31) / 32));
-  tide_route_kernel<<<1, kRouteThreads, route_smem, st>>>(rp);
-  CU_TRY(cudaGetLastError());
+  rp.pair_slot = c->pair_slot;
+  rp.cnt = cnt;
+  rp.cnt_next = cnt_next;
+  rp.list = c->list;
+  rp.mask = c->mask;
+  rp.g_cnt = c->g_cnt;
+  rp.zero_i = c->ffn_ctrl;
+  rp.n_zero = 1 + c->max_entries;
+  {
+    const dim3 grid((E + kRouterWarps - 1) / kRouterWarps, std::max(1, (N + rp.tpc - 1) / rp.tpc));
+    cudaError_t le;
+    const int epl = route_epl(E);
+#define ROUTE_LAUNCH(TT, EP) \
+  le = launch_pdl(tide_route_kernel<TT, EP>, grid, dim3(kRouteThreads), 0, st, rp)
+#define ROUTE_DISPATCH(TT)                     \
+    switch (epl) {                             \
+      case 1: ROUTE_LAUNCH(TT, 1); break;      \
+      case 2: ROUTE_LAUNCH(TT, 2); break;      \
+      case 4: ROUTE_LAUNCH(TT, 4); break;      \
+      case 8: ROUTE_LAUNCH(TT, 8); break;      \
+      case 16: ROUTE_LAUNCH(TT, 16); break;    \
+      default: ROUTE_LAUNCH(TT, 32); break;    \
+    }
+    if (c->bf16) {
+      ROUTE_DISPATCH(__nv_bfloat16)
+    } else {
+      ROUTE_DISPATCH(float)
+    }
+#undef ROUTE_DISPATCH
+#undef ROUTE_LAUNCH
+    CU_TRY(le);
+    c->launches++;
+  }
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
+
+  // ---------------- a4/a5 bookkeeping (placement, buckets, pos, info)
   if (pool_mode) {
+    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, st);
+    if (s != TIDE_OK) return s;
     CU_TRY(cudaMemcpyAsync(c->h_info, c->info, c->info_bytes, cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaEventRecord(c->ev_info, st));
+  } else {
+    CU_TRY(cudaEventRecord(c->ev_route, st));
+    CU_TRY(cudaStreamWaitEvent(c->side, c->ev_route, 0));
+    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, c->side);
+    if (s != TIDE_OK) return s;
+    CU_TRY(cudaEventRecord(c->ev_book, c->side));
   }
-  // ---------------- a5 gather, a7 FFN over experts already in HBM (+ shared)
+  if (c->timing) {
+    CU_TRY(cudaEventRecord(rec.ev[2], st));
+    CU_TRY(cudaEventRecord(rec.ev[3], st));
+  }
+  // ---------------- a7/a9 FFN over the hit experts already in HBM (+ shared expert)
   if (N > 0) {
-    if (c->bf16)
-      tide_gather_kernel<__nv_bfloat16><<<N, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(x), c->pos, c->info,
-          static_cast<__nv_bfloat16*>(c->x_perm), N, k, H, shared ? 1 : 0);
-    else
-      tide_gather_kernel<float><<<N, 256, 0, st>>>(static_cast<const float*>(x), c->pos, c->info,
-                                                   static_cast<float*>(c->x_perm), N, k, H,
-                                                   shared ? 1 : 0);
-    CU_TRY(cudaGetLastError());
-    s = launch_ffn(c, c->entries, &c->info->n_entries, &c->info->sched, c->done, st);
+    s = launch_ffn(c, cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
+                   c->ffn_ctrl + 1, N, st);
     if (s != TIDE_OK) return s;
   }
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
 
-  int copies = 0, staged_entries = 0;
+  int streamed = 0, copies = 0;
+  int64_t weight_bytes = 0;
   const RouteInfo* hinfo = nullptr;
-  if (pool_mode) {
+  if (pool_mode) {  // ---------------- a6 + a8
     CU_TRY(cudaEventRecord(c->ev_gemm1, st));
     CU_TRY(cudaEventSynchronize(c->ev_info));
     hinfo = static_cast<const RouteInfo*>(c->h_info);
     if (hinfo->status != 0)
       return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
                   step, capacity);
-    const int* hi = reinterpret_cast<const int*>(hinfo + 1);
-    const int* miss_e = hi;
-    const int* miss_off = miss_e + E;
-    const int* miss_m = miss_off + E;
-    const int* hits = miss_m + E;
-    const uint8_t* pl = reinterpret_cast<const uint8_t*>(hits + E);
-    const bool lazy = (c->d.flags & TIDE_LAZY_PROMOTE) != 0;
-    const int C = c->capacity, S = c->staging, half = std::max(1, S / 2);
-    const uint8_t* master = static_cast<const uint8_t*>(w->host_master);
-    uint8_t* pool = static_cast<uint8_t*>(c->pool);
-    const size_t xb = c->expert_bytes;
-
-    // release slots of experts that left the resident set (R-12: no D2H)
-    std::vector<int> free_now, free_after_gemm1;
-    for (int sl = 0; sl < C; ++sl)
-      if (c->owner[sl] < 0) free_now.push_back(sl);
-    for (int e = 0; e < E; ++e) {
-      const int sl = c->slot_of[e];
-      if (sl >= 0 && !pl[e]) {
-        (hits[e] > 0 ? free_after_gemm1 : free_now).push_back(sl);
-        c->owner[sl] = -1;
-        c->slot_of[e] = -1;
-      }
-    }
-    // plan copies: hit misses in bucket order (resident-marked -> pool slot, else staging),
-    // then eager promotions without hits
-    struct Copy { int e, dst, off, m; bool after_gemm1, staged; };
-    std::vector<Copy> hit_copies, cold_copies;
-    size_t fn = 0, fa = 0;
-    auto take_slot = [&](bool& after) -> int {
-      if (fn < free_now.size()) { after = false; return free_now[fn++]; }
-      after = true;
-      return free_after_gemm1[fa++];
-    };
-    for (int i = 0; i < hinfo->n_miss; ++i) {
-      const int e = miss_e[i];
-      Copy cp{e, -1, miss_off[i], miss_m[i], false, false};
-      if (pl[e]) {
-        cp.dst = take_slot(cp.after_gemm1);
-        c->owner[cp.dst] = e;
-        c->slot_of[e] = cp.dst;
-      } else {
-        cp.staged = true;
-      }
-      hit_copies.push_back(cp);
-    }
-    if (!lazy) {
-      for (int e = 0; e < E; ++e)
-        if (pl[e] && c->slot_of[e] < 0 && hits[e] == 0) {
-          Copy cp{e, -1, 0, 0, false, false};
-          cp.dst = take_slot(cp.after_gemm1);
-          c->owner[cp.dst] = e;
-          c->slot_of[e] = cp.dst;
-          cold_copies.push_back(cp);
-        }
-    }
-    // order: immediate pool copies and staged ones first, slots freed by GEMM#1 last
-    std::stable_partition(hit_copies.begin(), hit_copies.end(),
-                          [](const Copy& a) { return !a.after_gemm1; });
-    // chunks: <= half staging slots each
-    std::vector<std::pair<int, int>> chunks;  // [begin, end) into hit_copies
-    {
-      int b = 0, used = 0;
-      for (int i = 0; i < (int)hit_copies.size(); ++i) {
-        const bool boundary = (hit_copies[i].staged && used == half) ||
-                              (i > b && hit_copies[i].after_gemm1 && !hit_copies[i - 1].after_gemm1);
-        if (boundary) { chunks.push_back({b, i}); b = i; used = 0; }
-        if (hit_copies[i].staged) used++;
-      }
-      if (b < (int)hit_copies.size()) chunks.push_back({b, (int)hit_copies.size()});
-    }
-    if ((int)chunks.size() > c->max_chunks) return fail(TIDE_EINVAL, "too many staged chunks");
-    // work lists for the staged chunks (uploaded once, before the first chunk FFN)
-    int ne = 0;
-    std::vector<int> chunk_first(chunks.size() + 1, 0);
-    for (size_t ci = 0; ci < chunks.size(); ++ci) {
-      chunk_first[ci] = ne;
-      int stage_i = 0;
-      for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
-        Copy& cp = hit_copies[i];
-        if (cp.staged) cp.dst = C + (int)(ci % 2) * half + (stage_i++);
-        for (int t = 0; t < cp.m; t += kMaxTok)
-          c->h_entries2[ne++] = make_int4(cp.dst, cp.off + t, std::min(kMaxTok, cp.m - t), 0);
-      }
-      c->h_ctrl2[2 * ci] = ne - chunk_first[ci];
-      c->h_ctrl2[2 * ci + 1] = 0;
-    }
-    chunk_first[chunks.size()] = ne;
-    staged_entries = ne;
-    int* h_done2 = c->h_ctrl2 + 2 * c->max_chunks;
-    for (int i = 0; i < ne; ++i) h_done2[i] = 0;
-    if (!chunks.empty()) {
-      CU_TRY(cudaMemcpyAsync(c->entries2, c->h_entries2, sizeof(int4) * ne, cudaMemcpyHostToDevice, st));
-      CU_TRY(cudaMemcpyAsync(c->ctrl2, c->h_ctrl2, sizeof(int) * 2 * chunks.size(),
-                             cudaMemcpyHostToDevice, st));
-      CU_TRY(cudaMemcpyAsync(c->done2, h_done2, sizeof(int) * ne, cudaMemcpyHostToDevice, st));
-    }
-    // a6: copies on the side stream; a8: FFN per chunk on the main stream
-    bool waited_gemm1 = false;
-    for (size_t ci = 0; ci < chunks.size(); ++ci) {
-      if (ci >= 2) CU_TRY(cudaStreamWaitEvent(c->side, c->ev_chunk_done[ci - 2], 0));
-      for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
-        const Copy& cp = hit_copies[i];
-        if (cp.after_gemm1 && !waited_gemm1) {
-          CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
-          waited_gemm1 = true;
-        }
-        CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
-                               cudaMemcpyHostToDevice, c->side));
-        copies++;
-      }
-      CU_TRY(cudaEventRecord(c->ev_chunk_ready[ci], c->side));
-      CU_TRY(cudaStreamWaitEvent(st, c->ev_chunk_ready[ci], 0));
-      s = launch_ffn(c, c->entries2 + chunk_first[ci], c->ctrl2 + 2 * ci, c->ctrl2 + 2 * ci + 1,
-                     c->done2 + chunk_first[ci], st);
-      if (s != TIDE_OK) return s;
-      CU_TRY(cudaEventRecord(c->ev_chunk_done[ci], st));
-    }
-    for (const Copy& cp : cold_copies) {
-      if (cp.after_gemm1 && !waited_gemm1) {
-        CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
-        waited_gemm1 = true;
-      }
-      CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
-                             cudaMemcpyHostToDevice, c->side));
-      copies++;
-    }
-    CU_TRY(cudaEventRecord(c->ev_side_done, c->side));
-    CU_TRY(cudaStreamWaitEvent(st, c->ev_side_done, 0));
-    // publish the slot map for the next step's route kernel
-    for (int e = 0; e < E; ++e) c->h_slot_of[e] = c->slot_of[e];
-    CU_TRY(cudaMemcpyAsync(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice, st));
+    s = pool_step(c, w, hinfo, N, st, &streamed, &copies, &weight_bytes);
+    if (s != TIDE_OK) return s;
   }
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
 
   // ---------------- a10 combine
   if (N > 0) {
-    dim3 grid(N, (H + 1023) / 1024);
+    const dim3 grid(N, (H + 511) / 512);
     if (c->bf16)
-      tide_combine_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-          c->y_perm, c->gates, c->pos, c->info, static_cast<__nv_bfloat16*>(out), N, k, H,
-          shared ? 1 : 0);
+      CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
+                        (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
+                        (const int*)c->pair_slot, (const int*)c->off,
+                        static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0));
     else
-      tide_combine_kernel<float><<<grid, 256, 0, st>>>(c->y_perm, c->gates, c->pos, c->info,
-                                                       static_cast<float*>(out), N, k, H,
-                                                       shared ? 1 : 0);
-    CU_TRY(cudaGetLastError());
+      CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), 0, st,
+                        (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
+                        (const int*)c->pair_slot, (const int*)c->off, static_cast<float*>(out),
+                        N, k, H, shared ? 1 : 0));
+    c->launches++;
+  }
+  if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4/a5 outputs
+  if (c->timing) {
+    CU_TRY(cudaEventRecord(rec.ev[6], st));
+    rec.launches = c->launches - launches0;
+    rec.ffn_launches = c->ffn_launches - ffn0;
+    c->pending.push_back(rec);
   }
   if (dbg) {
     if (dbg->topk_idx) CU_TRY(cudaMemcpyAsync(dbg->topk_idx, c->topk, sizeof(int) * N * k, cudaMemcpyDeviceToDevice, st));
@@ -650,17 +808,58 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   if (stats) {
     RouteInfo local;
     if (!pool_mode) {
+      std::vector<int> hits(E);
       CU_TRY(cudaMemcpyAsync(&local, c->info, sizeof(RouteInfo), cudaMemcpyDeviceToHost, st));
+      CU_TRY(cudaMemcpyAsync(hits.data(), c->info + 1, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
       CU_TRY(cudaStreamSynchronize(st));
       hinfo = &local;
       if (local.status != 0)
         return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
                     step, capacity);
+      for (int e = 0; e < E; ++e)
+        weight_bytes += (int64_t)c->expert_bytes * ((hits[e] + kMaxTok - 1) / kMaxTok);
     } else {
       CU_TRY(cudaStreamSynchronize(st));
     }
-    fill_stats(c, hinfo, N, copies, hinfo->n_entries + staged_entries, stats);
+    if (shared) weight_bytes += (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok);
+    fill_stats(c, hinfo, N, streamed, copies, weight_bytes, stats);
   }
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_set_timing(tide_ctx* c, int32_t enable) {
+  if (!c) return fail(TIDE_EINVAL, "ctx is null");
+  tide_phase_times t;
+  tide_status s = tide_ctx_get_timing(c, &t);  // drain
+  if (s != TIDE_OK) return s;
+  c->acc = tide_phase_times{};
+  c->timing = enable != 0;
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_get_timing(tide_ctx* c, tide_phase_times* out) {
+  if (!c || !out) return fail(TIDE_EINVAL, "null argument");
+  CU_TRY(cudaSetDevice(c->device));
+  for (auto& r : c->pending) {
+    CU_TRY(cudaEventSynchronize(r.ev[6]));
+    float ms[6];
+    for (int i = 0; i < 6; ++i) CU_TRY(cudaEventElapsedTime(&ms[i], r.ev[i], r.ev[i + 1]));
+    c->acc.router_ms += ms[0];
+    c->acc.route_ms += ms[1];
+    c->acc.gather_ms += ms[2];
+    c->acc.ffn_ms += ms[3];
+    c->acc.staged_ms += ms[4];
+    c->acc.combine_ms += ms[5];
+    float tot;
+    CU_TRY(cudaEventElapsedTime(&tot, r.ev[0], r.ev[6]));
+    c->acc.total_ms += tot;
+    c->acc.steps += 1;
+    c->acc.launches += r.launches;
+    c->acc.ffn_launches += r.ffn_launches;
+    for (cudaEvent_t e : r.ev) c->ev_pool.push_back(e);
+  }
+  c->pending.clear();
+  *out = c->acc;
   return TIDE_OK;
 }
 

@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EP
 
 EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert_elems",
             "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
-            "tide_moe_step")
+            "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing")
 
 
 class TideError(RuntimeError):
@@ -62,6 +62,15 @@ class StepDebug(ctypes.Structure):
                                                 "logits")]
 
 
+class PhaseTimes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("router_ms", "route_ms", "gather_ms", "ffn_ms",
+                                                "staged_ms", "combine_ms", "total_ms")] + [
+        ("steps", ctypes.c_int64), ("launches", ctypes.c_int64), ("ffn_launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -88,6 +97,8 @@ def lib():
             ctypes.POINTER(ExpertWeights), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.POINTER(StepStats), ctypes.POINTER(StepDebug), ctypes.c_void_p]
+        L.tide_ctx_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.tide_ctx_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(PhaseTimes)]
         _lib = L
     return _lib
 
@@ -162,6 +173,15 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def set_timing(self, enable: bool = True):
+        """tide_ctx_set_timing: per-phase CUDA-event timing on the step stream."""
+        _check(lib().tide_ctx_set_timing(self.handle, int(enable)))
+
+    def timing(self) -> dict:
+        t = PhaseTimes()
+        _check(lib().tide_ctx_get_timing(self.handle, ctypes.byref(t)))
+        return t.as_dict()
 
     def moe_step(self, block_hidden, router_w, *, device_all=None, host_master=None,
                  shared_w=None, placement, step: int, interval: int, capacity: int | None = None,

@@ -278,3 +278,33 @@ def block_hidden_torch(shape: Shape, seed: int, layer: int, device, steps: int |
         x[:, 0] = 1.0
         out[t] = x.to(dt)
     return out
+
+
+def _uniform_torch_keys(keys, n: int, bound: float, device, out_dtype):
+    """Row e of the result == uniform_torch(keys[e], n, bound): one hash stream per key."""
+    import torch
+    kt = torch.tensor(keys, dtype=torch.int64, device=device)[:, None]
+    idx = torch.arange(n, dtype=torch.int64, device=device)[None, :]
+    h = _fmix_t((idx * _GOLD + kt) & M32)
+    f32 = lambda v: torch.tensor(v, dtype=torch.float32, device=device)  # noqa: E731
+    u = (h >> 8).to(torch.float32) * f32(2.0 ** -24)
+    return ((u * f32(2.0) - f32(1.0)) * f32(bound)).to(out_dtype)
+
+
+def layer_torch(shape: Shape, seed: int, layer: int, device, chunk: int = 32):
+    """Device twin of layer_np: (wr [E,H], wg [E,F,H], wu [E,F,H], wd [E,H,F], shared|None),
+    bit-identical to the host generator, generated `chunk` experts at a time."""
+    import torch
+    dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
+    E, H, F = shape.num_experts, shape.hidden, shape.ffn
+    wg = torch.empty(E, F, H, dtype=dt, device=device)
+    wu = torch.empty(E, F, H, dtype=dt, device=device)
+    wd = torch.empty(E, H, F, dtype=dt, device=device)
+    for e0 in range(0, E, chunk):
+        es = range(e0, min(E, e0 + chunk))
+        for out, tag, n, fan in ((wg, T_WG, F * H, H), (wu, T_WU, F * H, H), (wd, T_WD, H * F, F)):
+            keys = [_key(seed, layer, tag, e) for e in es]
+            out[e0:e0 + len(es)] = _uniform_torch_keys(keys, n, math.sqrt(3.0 / fan), device,
+                                                       dt).view(len(es), *out.shape[1:])
+    shared = shared_torch(shape, seed, layer, device) if shape.shared_expert else None
+    return router_torch(shape, seed, layer, device), wg, wu, wd, shared
