@@ -399,20 +399,31 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            int H, int shared) {
   pdl_wait();
   pdl_trigger();
-  const int n = blockIdx.x;
+  const int n = blockIdx.x, lane = threadIdx.x & 31;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  if (c >= H) return;
+  // lane j < k fetches pair j's row and gate (one round of independent loads), then the
+  // y rows are read with all loads of an unrolled group in flight
+  int r_j = 0;
+  float g_j = 0.f;
+  if (lane < k) {
+    const int q = n * k + lane;
+    r_j = __ldcg(off + __ldcg(topk + q)) + __ldcg(pair_slot + q);
+    g_j = __ldcg(gates + q);
+  }
+  const bool valid = c < H;  // (lanes stay converged for the shuffles)
+  const int cc = valid ? c : 0;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
   for (int j = 0; j < k; ++j) {
-    const int q = n * k + j;
-    const float g = __ldcg(gates + q);
-    const int r = __ldcg(off + __ldcg(topk + q)) + __ldcg(pair_slot + q);
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)r * H + c));
+    const int r = __shfl_sync(0xffffffffu, r_j, j);
+    const float g = __shfl_sync(0xffffffffu, g_j, j);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)r * H + cc));
     acc.x = fmaf(g, v.x, acc.x);
     acc.y = fmaf(g, v.y, acc.y);
     acc.z = fmaf(g, v.z, acc.z);
     acc.w = fmaf(g, v.w, acc.w);
   }
+  if (!valid) return;
   if (shared) {
     const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(N * k + n) * H + c));
     acc.x += v.x;
