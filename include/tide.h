@@ -132,6 +132,8 @@ typedef struct {
   int32_t* order;    /* [E] expert at each bucket position                        */
   int32_t* offsets;  /* [E + 1] first row of each bucket position                 */
   float* logits;     /* [N, E] fp32 router logits                                 */
+  uint64_t* route_trace; /* [4 * route CTAs] %globaltimer ns per route-kernel CTA:
+                            start, phase 1 done, phase 2 start, phase 2 done (0 = n/a) */
 } tide_step_debug;
 
 typedef struct tide_ctx tide_ctx;

@@ -78,6 +78,7 @@ struct RouteParams {
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
   int n_zero;
+  unsigned long long* trace;  // debug: 4 timestamps per CTA (nullable)
 };
 
 struct BookParams {
@@ -148,6 +149,9 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
   pdl_wait();     // X may be written by the previous kernel in the stream
   pdl_trigger();  // let the FFN grid start its prologue
+  unsigned long long* tr =
+      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     for (int i = tid; i < E; i += blockDim.x) p.cnt_next[i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
@@ -207,13 +211,17 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   __threadfence();
   __syncthreads();
   if (tid == 0) {
+    if (tr) tr[1] = globaltimer_ns();
     __threadfence();
     s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
   if (!s_flag) return;
   __threadfence();
-  if (tid == 0) p.g_cnt[blockIdx.y] = 0;
+  if (tid == 0) {
+    p.g_cnt[blockIdx.y] = 0;
+    if (tr) tr[2] = globaltimer_ns();
+  }
 
   // ================= phase 2: top-k of this token group (a2) + histogram (a3)
   // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
@@ -279,6 +287,10 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
       p.pair_slot[(size_t)n * k + lane] = slot;
       atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
     }
+  }
+  if (tr) {
+    __syncthreads();
+    if (tid == 0) tr[3] = globaltimer_ns();
   }
 }
 

@@ -708,6 +708,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   rp.g_cnt = c->g_cnt;
   rp.zero_i = c->ffn_ctrl;
   rp.n_zero = 1 + c->max_entries;
+  rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
+                                       : nullptr;
   {
     const dim3 grid((E + kRouterWarps - 1) / kRouterWarps, std::max(1, (N + rp.tpc - 1) / rp.tpc));
     cudaError_t le;

@@ -59,7 +59,7 @@ class StepStats(ctypes.Structure):
 
 class StepDebug(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("topk_idx", "gates", "pos", "order", "offsets",
-                                                "logits")]
+                                                "logits", "route_trace")]
 
 
 class PhaseTimes(ctypes.Structure):
@@ -212,7 +212,9 @@ class Context:
                      "pos": torch.empty(N, k, dtype=torch.int32, device=dev),
                      "order": torch.empty(E, dtype=torch.int32, device=dev),
                      "offsets": torch.empty(E + 1, dtype=torch.int32, device=dev),
-                     "logits": torch.empty(N, E, dtype=torch.float32, device=dev)}
+                     "logits": torch.empty(N, E, dtype=torch.float32, device=dev),
+                     "route_trace": torch.zeros(4 * ((E + 7) // 8) * max(1, (N + 7) // 4),
+                                                dtype=torch.int64, device=dev)}
             dbg = StepDebug(*(dbg_t[n].data_ptr() for n, _ in StepDebug._fields_))
         _check(lib().tide_moe_step(
             self.handle, _ptr(block_hidden), N, _ptr(router_w), ctypes.byref(w), _ptr(placement),
