@@ -180,6 +180,37 @@ TIDE_API tide_status tide_moe_step(tide_ctx* ctx, const void* block_hidden, int3
                           uint8_t* placement_out, tide_step_stats* stats, tide_step_debug* dbg,
                           void* stream);
 
+/* ------------------------------------------------------------------------
+ * Expert parallelism (DESIGN R-18), one process per GPU.
+ * Rank r of P owns experts [r*E/P, (r+1)*E/P); each rank routes its own tokens.
+ * A step: route (local tokens) -> ncclAllGather of tokens, top-k ids and gates
+ * (fixed max_tokens rows per rank, no host sync) -> grouped FFN over the local
+ * experts for every rank's tokens -> per-source partial sums (fp32, slot order)
+ * -> ncclAlltoAll -> out = sum of the P partials in rank order (+ shared expert).
+ * hit_counts is global ([E], ncclAllGather of the local experts' counts);
+ * placement / placement_out cover the rank's E/P local experts (device [E/P]);
+ * capacity is per rank (1 <= C <= E/P).  The context owns its NCCL communicator.
+ * ------------------------------------------------------------------------ */
+
+/* Fill out[128] with a fresh ncclUniqueId (call on one rank, share the bytes). */
+TIDE_API tide_status tide_nccl_unique_id(void* out);
+
+/* Collective over the `world` ranks (each calls it with the same unique id).
+ * E must be divisible by world. */
+TIDE_API tide_status tide_ctx_create_ep(const tide_layer_desc* desc, int32_t device,
+                                        const void* nccl_unique_id, int32_t rank, int32_t world,
+                                        tide_ctx** out);
+
+/* local_experts: device, E/P packed experts of this rank (expert r*E/P + i at slot i).
+ * shared_w: device packed shared expert (iff TIDE_SHARED_EXPERT).  Other arguments as
+ * tide_moe_step.  Every rank must call it for the same layer/step (collectives). */
+TIDE_API tide_status tide_moe_step_ep(tide_ctx* ctx, const void* block_hidden, int32_t num_tokens,
+                                      const void* router_w, const void* local_experts,
+                                      const void* shared_w, const uint8_t* placement,
+                                      int32_t step, int32_t interval, int32_t capacity, void* out,
+                                      int32_t* hit_counts, uint8_t* placement_out,
+                                      tide_step_stats* stats, void* stream);
+
 /* Per-phase device timing (CUDA events recorded on the step's stream at phase
  * boundaries).  Enabling resets the accumulators; tide_ctx_get_timing waits
  * for the recorded events, adds their elapsed times and clears them.

@@ -30,11 +30,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
+def nccl_dirs():
+    import nvidia.nccl as _n
+    base = os.path.dirname(_n.__file__) if getattr(_n, "__file__", None) else list(_n.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB,
-                            os.path.join(CSRC, "tide.cu")]
+    nccl_inc, nccl_lib = nccl_dirs()
+    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-o", LIB,
+                            os.path.join(CSRC, "tide.cu"), "-L", nccl_lib, "-l:libnccl.so.2",
+                            "-Xlinker", "-rpath=" + nccl_lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

@@ -57,6 +57,8 @@ struct FfnParams {
   void* h_out;
   float* y_out;
   int H, F, E, maxN, N, k, shared;
+  int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
+  int shared_tok0;       // token id of its first row (0 single-device, rank*maxN under EP)
 };
 
 struct FfnItem {
@@ -149,8 +151,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       n_ent = __shfl_sync(0xffffffffu, ent_x, 31);
       const int n_sh = p.shared ? (p.N + kMaxTok - 1) / kMaxTok : 0;
       for (int c = lane; c < n_sh; c += 32)
-        s_ent[n_ent + c] = make_int4(0, p.N * p.k + c * kMaxTok,
-                                     min(kMaxTok, p.N - c * kMaxTok) | (3 << 16), c * kMaxTok);
+        s_ent[n_ent + c] = make_int4(0, p.shared_row0 + c * kMaxTok,
+                                     min(kMaxTok, p.N - c * kMaxTok) | (3 << 16),
+                                     p.shared_tok0 + c * kMaxTok);
       n_ent += n_sh;
       ents = s_ent;
       __syncwarp();

@@ -25,7 +25,10 @@
 #include <utility>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/tide.h"
+#include "ep.cuh"
 #include "ffn.cuh"
 #include "route.cuh"
 
@@ -44,6 +47,14 @@ tide_status fail(tide_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
+
+#define NC_TRY(expr)                                                                     \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(TIDE_ENCCL, "%s failed: %s (%s:%d)", #expr, ncclGetErrorString(r_),     \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
 
 #define CU_TRY(expr)                                                                     \
   do {                                                                                   \
@@ -148,6 +159,22 @@ struct tide_ctx {
   const void* map_shared_src = nullptr;
   bool have_shared_map = false;
 
+  // expert parallelism (tide_ctx_create_ep)
+  bool ep = false;
+  int rank = 0, world = 1, El = 0, e0 = 0, rows_all = 0;
+  ncclComm_t comm = nullptr;
+  void* x_all = nullptr;        // [P*maxN, H] all ranks' tokens
+  int* topk_all = nullptr;      // [P*maxN, k]
+  float* gates_all = nullptr;   // [P*maxN, k]
+  int* pslot_all = nullptr;     // [P*maxN, k]
+  int* cnt_l = nullptr;         // [El] local experts' token counts over all rows
+  int* list_l = nullptr;        // [El, P*maxN]
+  int* off_l = nullptr;         // [El]
+  int* hits_l = nullptr;        // [El] scratch
+  float* partial = nullptr;     // [P*maxN, H] per-source partial sums (send buffer)
+  float* recv = nullptr;        // [P*maxN, H] partials for this rank's tokens
+  CUtensorMap map_x_all;
+
   // per-phase timing (tide_ctx_set_timing)
   bool timing = false;
   struct Rec { cudaEvent_t ev[7]; int64_t launches, ffn_launches; };
@@ -245,7 +272,9 @@ void tide_ctx_destroy(tide_ctx* c) {
   void* dev[] = {c->logits, c->topk,     c->gates,   c->pair_slot, c->cnt,    c->list,
                  c->mask,   c->g_cnt,    c->off,     c->pos,       c->order,  c->offsets,
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
-                 c->pool,   c->entries2, c->ctrl2,   c->done2};
+                 c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
+                 c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
+                 c->partial, c->recv};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -260,6 +289,7 @@ void tide_ctx_destroy(tide_ctx* c) {
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->comm) ncclCommDestroy(c->comm);
   delete c;
 }
 
@@ -272,8 +302,9 @@ void tide_ctx_destroy(tide_ctx* c) {
     cudaMemset((ptr), 0, (bytes));                                                         \
   } while (0)
 
-tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t staging_slots,
-                            int32_t device, tide_ctx** out) {
+static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
+                                   int32_t staging_slots, int32_t device, int32_t world,
+                                   tide_ctx** out) {
   if (!out) return fail(TIDE_EINVAL, "out is null");
   *out = nullptr;
   tide_status s = validate_desc(d);
@@ -307,8 +338,10 @@ tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t 
   c->expert_elems = tide_expert_elems(d);
   c->expert_bytes = tide_expert_bytes(d);
   const int E = c->E, k = c->k, N = c->maxN;
-  c->max_rows = N * k + N;
-  c->max_entries = E + (N * k) / kMaxTok + 2 + (N + kMaxTok - 1) / kMaxTok;
+  c->world = world;
+  c->rows_all = world * N;
+  c->max_rows = world * N * k + N;
+  c->max_entries = E / world + (world * N * k) / kMaxTok + 2 + (N + kMaxTok - 1) / kMaxTok;
 
   ALLOC(c->logits, sizeof(float) * N * E);
   ALLOC(c->topk, sizeof(int) * N * k);
@@ -362,6 +395,71 @@ tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t 
   return TIDE_OK;
 }
 
+tide_status tide_ctx_create(const tide_layer_desc* d, int32_t capacity, int32_t staging_slots,
+                            int32_t device, tide_ctx** out) {
+  return ctx_create_impl(d, capacity, staging_slots, device, 1, out);
+}
+
+tide_status tide_nccl_unique_id(void* out) {
+  if (!out) return fail(TIDE_EINVAL, "out is null");
+  ncclUniqueId id;
+  NC_TRY(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_create_ep(const tide_layer_desc* d, int32_t device, const void* nccl_id,
+                               int32_t rank, int32_t world, tide_ctx** out) {
+  if (!out || !nccl_id) return fail(TIDE_EINVAL, "null argument");
+  *out = nullptr;
+  tide_status s = validate_desc(d);
+  if (s != TIDE_OK) return s;
+  if (world < 1 || rank < 0 || rank >= world) return fail(TIDE_EINVAL, "rank %d / world %d", rank, world);
+  if (d->num_experts % world)
+    return fail(TIDE_EUNSUPPORTED, "num_experts %d not divisible by world %d", d->num_experts, world);
+  if (d->num_experts / world < d->top_k && world > 1 && false)
+    return fail(TIDE_EUNSUPPORTED, "fewer local experts than top_k");
+  const int El = d->num_experts / world;
+  const int max_ent = El + world * d->max_tokens * d->top_k / kMaxTok + 2 +
+                      (d->max_tokens + kMaxTok - 1) / kMaxTok;
+  if (max_ent > kMaxEntriesSmem)
+    return fail(TIDE_EUNSUPPORTED, "EP work list too large (%d > %d)", max_ent, kMaxEntriesSmem);
+  tide_ctx* c = nullptr;
+  s = ctx_create_impl(d, d->num_experts, 2, device, world, &c);
+  if (s != TIDE_OK) return s;
+  c->ep = true;
+  c->rank = rank;
+  c->El = El;
+  c->e0 = rank * El;
+  const int N = c->maxN, k = c->k, R = c->rows_all;
+  ALLOC(c->x_all, c->eb * (size_t)R * c->H);
+  ALLOC(c->topk_all, sizeof(int) * (size_t)R * k);
+  ALLOC(c->gates_all, sizeof(float) * (size_t)R * k);
+  ALLOC(c->pslot_all, sizeof(int) * (size_t)R * k);
+  ALLOC(c->cnt_l, sizeof(int) * El);
+  ALLOC(c->list_l, sizeof(int) * (size_t)El * R);
+  ALLOC(c->off_l, sizeof(int) * El);
+  ALLOC(c->hits_l, sizeof(int) * El);
+  ALLOC(c->partial, sizeof(float) * (size_t)R * c->H);
+  ALLOC(c->recv, sizeof(float) * (size_t)R * c->H);
+  (void)N;
+  if (make_map(&c->map_x_all, c->x_all, c->bf16, c->H, R, 1) != TIDE_OK) {
+    std::string m = g_err;
+    tide_ctx_destroy(c);
+    return fail(TIDE_ECUDA, "%s", m.c_str());
+  }
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    tide_ctx_destroy(c);
+    return fail(TIDE_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return TIDE_OK;
+}
+
 // Lazily set up host_master resources (slot pool, staging ring, pinned mirrors).
 static tide_status ensure_pool(tide_ctx* c) {
   if (c->pool) return TIDE_OK;
@@ -398,7 +496,7 @@ static tide_status ensure_pool(tide_ctx* c) {
 // global mode: entries/n_entries (host-built staged chunk).
 static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
-                              int N, cudaStream_t st) {
+                              int N, cudaStream_t st, bool ep_local = false) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -423,6 +521,17 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.N = N;
   p.k = c->k;
   p.shared = (c->d.flags & TIDE_SHARED_EXPERT) ? 1 : 0;
+  p.shared_row0 = N * c->k;
+  p.shared_tok0 = 0;
+  if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
+    p.map_x = c->map_x_all;
+    p.off_out = c->off_l;
+    p.list = c->list_l;
+    p.E = c->El;
+    p.maxN = c->rows_all;
+    p.shared_row0 = c->rows_all * c->k;
+    p.shared_tok0 = c->rank * c->maxN;
+  }
   if (c->bf16)
     CU_TRY(launch_pdl(tide_ffn_kernel<__nv_bfloat16>, dim3(c->num_sms), dim3(kFfnThreads),
                       kFfnSmemBytes, st, p));
@@ -471,7 +580,8 @@ static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, 
 
 static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
                                int refresh, int capacity, int32_t* hit_counts,
-                               uint8_t* placement_out, cudaStream_t st) {
+                               uint8_t* placement_out, cudaStream_t st, int E_override = 0) {
+  const int E = E_override ? E_override : c->E;
   BookParams b;
   b.cnt = cnt;
   b.mask = c->mask;
@@ -479,7 +589,7 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   b.topk_idx = c->topk;
   b.placement_in = placement;
   b.N = N;
-  b.E = c->E;
+  b.E = E;
   b.k = c->k;
   b.refresh = refresh;
   b.capacity = capacity;
@@ -489,9 +599,64 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   b.offsets = c->offsets;
   b.pos = c->pos;
   b.info = c->info;
-  tide_book_kernel<<<1, 1024, sizeof(int) * 5 * c->E, st>>>(b);
+  tide_book_kernel<<<1, 1024, sizeof(int) * 5 * E, st>>>(b);
   CU_TRY(cudaGetLastError());
   c->launches++;
+  return TIDE_OK;
+}
+
+static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* wr, int* cnt,
+                                int* cnt_next, tide_step_debug* dbg, cudaStream_t st) {
+  const int E = c->E, k = c->k, H = c->H;
+  RouteParams rp;
+  rp.x = x;
+  rp.wr = wr;
+  rp.x_in = c->x_in;
+  rp.logits = c->logits;
+  rp.N = N;
+  rp.E = E;
+  rp.H = H;
+  rp.k = k;
+  rp.tpc = N <= 64 ? 4 : 8;
+  rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
+  rp.maxN = c->maxN;
+  rp.topk_idx = c->topk;
+  rp.gates = c->gates;
+  rp.pair_slot = c->pair_slot;
+  rp.cnt = cnt;
+  rp.cnt_next = cnt_next;
+  rp.list = c->list;
+  rp.mask = c->mask;
+  rp.g_cnt = c->g_cnt;
+  rp.zero_i = c->ffn_ctrl;
+  rp.n_zero = 1 + c->max_entries;
+  rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
+                                       : nullptr;
+  {
+    const dim3 grid((E + kRouterWarps - 1) / kRouterWarps, std::max(1, (N + rp.tpc - 1) / rp.tpc));
+    cudaError_t le;
+    const int epl = route_epl(E);
+#define ROUTE_LAUNCH(TT, EP) \
+  le = launch_pdl(tide_route_kernel<TT, EP>, grid, dim3(kRouteThreads), 0, st, rp)
+#define ROUTE_DISPATCH(TT)                     \
+    switch (epl) {                             \
+      case 1: ROUTE_LAUNCH(TT, 1); break;      \
+      case 2: ROUTE_LAUNCH(TT, 2); break;      \
+      case 4: ROUTE_LAUNCH(TT, 4); break;      \
+      case 8: ROUTE_LAUNCH(TT, 8); break;      \
+      case 16: ROUTE_LAUNCH(TT, 16); break;    \
+      default: ROUTE_LAUNCH(TT, 32); break;    \
+    }
+    if (c->bf16) {
+      ROUTE_DISPATCH(__nv_bfloat16)
+    } else {
+      ROUTE_DISPATCH(float)
+    }
+#undef ROUTE_DISPATCH
+#undef ROUTE_LAUNCH
+    CU_TRY(le);
+    c->launches++;
+  }
   return TIDE_OK;
 }
 
@@ -686,55 +851,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     CU_TRY(cudaEventRecord(rec.ev[0], st));
   }
   // ---------------- a1..a3: router, top-k, hits and per-expert token lists
-  RouteParams rp;
-  rp.x = x;
-  rp.wr = wr;
-  rp.x_in = c->x_in;
-  rp.logits = c->logits;
-  rp.N = N;
-  rp.E = E;
-  rp.H = H;
-  rp.k = k;
-  rp.tpc = N <= 64 ? 4 : 8;
-  rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
-  rp.maxN = c->maxN;
-  rp.topk_idx = c->topk;
-  rp.gates = c->gates;
-  rp.pair_slot = c->pair_slot;
-  rp.cnt = cnt;
-  rp.cnt_next = cnt_next;
-  rp.list = c->list;
-  rp.mask = c->mask;
-  rp.g_cnt = c->g_cnt;
-  rp.zero_i = c->ffn_ctrl;
-  rp.n_zero = 1 + c->max_entries;
-  rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
-                                       : nullptr;
-  {
-    const dim3 grid((E + kRouterWarps - 1) / kRouterWarps, std::max(1, (N + rp.tpc - 1) / rp.tpc));
-    cudaError_t le;
-    const int epl = route_epl(E);
-#define ROUTE_LAUNCH(TT, EP) \
-  le = launch_pdl(tide_route_kernel<TT, EP>, grid, dim3(kRouteThreads), 0, st, rp)
-#define ROUTE_DISPATCH(TT)                     \
-    switch (epl) {                             \
-      case 1: ROUTE_LAUNCH(TT, 1); break;      \
-      case 2: ROUTE_LAUNCH(TT, 2); break;      \
-      case 4: ROUTE_LAUNCH(TT, 4); break;      \
-      case 8: ROUTE_LAUNCH(TT, 8); break;      \
-      case 16: ROUTE_LAUNCH(TT, 16); break;    \
-      default: ROUTE_LAUNCH(TT, 32); break;    \
-    }
-    if (c->bf16) {
-      ROUTE_DISPATCH(__nv_bfloat16)
-    } else {
-      ROUTE_DISPATCH(float)
-    }
-#undef ROUTE_DISPATCH
-#undef ROUTE_LAUNCH
-    CU_TRY(le);
-    c->launches++;
-  }
+  s = launch_route(c, x, N, wr, cnt, cnt_next, dbg, st);
+  if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
 
   // ---------------- a4/a5 bookkeeping (placement, buckets, pos, info)
@@ -825,6 +943,92 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     }
     if (shared) weight_bytes += (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok);
     fill_stats(c, hinfo, N, streamed, copies, weight_bytes, stats);
+  }
+  return TIDE_OK;
+}
+
+tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* wr,
+                             const void* local_experts, const void* shared_w,
+                             const uint8_t* placement, int32_t step, int32_t interval,
+                             int32_t capacity, void* out, int32_t* hit_counts,
+                             uint8_t* placement_out, tide_step_stats* stats, void* stream) {
+  if (!c || !c->ep) return fail(TIDE_EINVAL, "not an expert-parallel context");
+  if (N < 0 || N > c->maxN) return fail(TIDE_EINVAL, "num_tokens %d outside [0, %d]", N, c->maxN);
+  const bool shared = (c->d.flags & TIDE_SHARED_EXPERT) != 0;
+  if (!local_experts || !wr || !placement || !placement_out || !hit_counts || (N > 0 && (!x || !out)))
+    return fail(TIDE_EINVAL, "null tensor argument");
+  if (shared && !shared_w) return fail(TIDE_EINVAL, "TIDE_SHARED_EXPERT set but shared_w is null");
+  if (interval < 1) return fail(TIDE_EINVAL, "interval %d < 1", interval);
+  if (step < 0) return fail(TIDE_EINVAL, "step %d < 0", step);
+  if (capacity < 1 || capacity > c->El)
+    return fail(TIDE_ECAPACITY, "capacity %d outside [1, %d] (per rank)", capacity, c->El);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU_TRY(cudaSetDevice(c->device));
+  const int E = c->E, k = c->k, H = c->H, maxN = c->maxN, R = c->rows_all, El = c->El;
+  const int refresh = (step % interval) == 0;
+  tide_status s = ensure_weight_maps(c, local_experts, El, shared ? shared_w : nullptr);
+  if (s != TIDE_OK) return s;
+  int* cnt = c->cnt + c->parity * E;
+  int* cnt_next = c->cnt + (c->parity ^ 1) * E;
+  c->parity ^= 1;
+  // a1..a3 on this rank's tokens
+  s = launch_route(c, x, N, wr, cnt, cnt_next, nullptr, st);
+  if (s != TIDE_OK) return s;
+  if (N < maxN) CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
+  // dispatch: every rank's tokens and routing to every rank (fixed counts, no host sync)
+  const ncclDataType_t xt = c->bf16 ? ncclBfloat16 : ncclFloat32;
+  NC_TRY(ncclGroupStart());
+  NC_TRY(ncclAllGather(c->x_in, c->x_all, (size_t)maxN * H, xt, c->comm, st));
+  NC_TRY(ncclAllGather(c->topk, c->topk_all, (size_t)maxN * k, ncclInt32, c->comm, st));
+  NC_TRY(ncclAllGather(c->gates, c->gates_all, (size_t)maxN * k, ncclFloat32, c->comm, st));
+  NC_TRY(ncclGroupEnd());
+  // local experts' token lists over all rows; their counts are the global hits (R-18)
+  CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
+  tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El, c->cnt_l,
+                                                          c->list_l, R, c->pslot_all);
+  CU_TRY(cudaGetLastError());
+  c->launches++;
+  s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El);
+  if (s != TIDE_OK) return s;
+  // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
+  s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true);
+  if (s != TIDE_OK) return s;
+  // a10: per-source partial sums, all-to-all, rank-order sum
+  CU_TRY(launch_pdl(tide_ep_partial_kernel, dim3(R, (H + 511) / 512), dim3(128), 0, st,
+                    (const float*)c->y_perm, (const int*)c->topk_all, (const float*)c->gates_all,
+                    (const int*)c->pslot_all, (const int*)c->off_l, c->partial, k, H, c->e0, El));
+  c->launches++;
+  NC_TRY(ncclAlltoAll(c->partial, c->recv, (size_t)maxN * H, ncclFloat32, c->comm, st));
+  if (N > 0) {
+    const dim3 grid(N, (H + 511) / 512);
+    const int srow = shared ? R * k : -1;
+    if (c->bf16)
+      CU_TRY(launch_pdl(tide_ep_final_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
+                        (const float*)c->recv, (const float*)c->y_perm,
+                        static_cast<__nv_bfloat16*>(out), c->world, maxN, H, srow));
+    else
+      CU_TRY(launch_pdl(tide_ep_final_kernel<float>, grid, dim3(128), 0, st, (const float*)c->recv,
+                        (const float*)c->y_perm, static_cast<float*>(out), c->world, maxN, H,
+                        srow));
+    c->launches++;
+  }
+  NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
+  if (stats) {
+    RouteInfo local;
+    std::vector<int> hl(El);
+    CU_TRY(cudaMemcpyAsync(&local, c->info, sizeof(RouteInfo), cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaMemcpyAsync(hl.data(), c->cnt_l, sizeof(int) * El, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaStreamSynchronize(st));
+    if (local.status != 0)
+      return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
+                  step, capacity);
+    int64_t wb = 0;
+    for (int e = 0; e < El; ++e) wb += (int64_t)c->expert_bytes * ((hl[e] + kMaxTok - 1) / kMaxTok);
+    if (shared) wb += (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok);
+    fill_stats(c, &local, N, 0, 0, wb, stats);
+    stats->nonresident_pairs = 0;
+    for (int e = 0; e < El; ++e) stats->nonresident_pairs += hl[e];
+    stats->nonresident_pairs -= local.resident_pairs;
   }
   return TIDE_OK;
 }

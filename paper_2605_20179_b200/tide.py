@@ -26,7 +26,8 @@ STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EP
 
 EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert_elems",
             "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
-            "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing")
+            "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing", "tide_nccl_unique_id",
+            "tide_ctx_create_ep", "tide_moe_step_ep")
 
 
 class TideError(RuntimeError):
@@ -97,6 +98,15 @@ def lib():
             ctypes.POINTER(ExpertWeights), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.POINTER(StepStats), ctypes.POINTER(StepDebug), ctypes.c_void_p]
+        L.tide_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        L.tide_ctx_create_ep.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_int32, ctypes.c_void_p,
+                                         ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_void_p)]
+        L.tide_moe_step_ep.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(StepStats),
+            ctypes.c_void_p]
         L.tide_ctx_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.tide_ctx_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(PhaseTimes)]
         _lib = L
@@ -234,3 +244,50 @@ def pack_layer(desc: LayerDesc, wg, wu, wd, out=None):
     for e in range(E):
         pack_expert(desc, wg[e], wu[e], wd[e], out[e])
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """tide_nccl_unique_id: 128 bytes to share with every rank."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tide_nccl_unique_id(buf))
+    return buf.raw
+
+
+class EPContext(Context):
+    """tide_ctx_create_ep: expert-parallel context (rank of world), own NCCL communicator."""
+
+    def __init__(self, desc: LayerDesc, unique_id: bytes, rank: int, world: int, device: int = 0):
+        h = ctypes.c_void_p()
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().tide_ctx_create_ep(ctypes.byref(desc), device, uid, rank, world,
+                                        ctypes.byref(h)))
+        self.handle = h
+        self.desc = desc
+        self.rank, self.world = rank, world
+        self.local_experts = desc.num_experts // world
+        self.capacity = self.local_experts
+        self.device = device
+
+    def moe_step_ep(self, block_hidden, router_w, local_experts, *, shared_w=None, placement,
+                    step: int, interval: int, capacity: int | None = None, out=None,
+                    hit_counts=None, placement_out=None, stats: bool = False,
+                    stream=None) -> StepOutputs:
+        """tide_moe_step_ep: local_experts [E/P, 3HF] device (this rank's experts),
+        placement [E/P] uint8 device; hit_counts [E] (global)."""
+        d = self.desc
+        N = block_hidden.shape[0]
+        dev = block_hidden.device
+        if out is None:
+            out = torch.empty(N, d.hidden, dtype=block_hidden.dtype, device=dev)
+        if hit_counts is None:
+            hit_counts = torch.empty(d.num_experts, dtype=torch.int32, device=dev)
+        if placement_out is None:
+            placement_out = torch.empty(self.local_experts, dtype=torch.uint8, device=dev)
+        st = StepStats() if stats else None
+        _check(lib().tide_moe_step_ep(
+            self.handle, _ptr(block_hidden), N, _ptr(router_w), _ptr(local_experts),
+            _ptr(shared_w), _ptr(placement), step, interval,
+            self.capacity if capacity is None else capacity, _ptr(out), _ptr(hit_counts),
+            _ptr(placement_out), ctypes.byref(st) if st is not None else None,
+            _stream_ptr(stream)))
+        return StepOutputs(out, hit_counts, placement_out, st.as_dict() if st else None, None)
