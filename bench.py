@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ep", action="store_true",
+                    help="expert parallelism over the ranks (tide_moe_step_ep) instead of replicas")
     return ap.parse_args()
 
 
@@ -164,29 +166,51 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     pool_mode = cap < E
     desc = tide.make_desc(E, k, H, F, N, tide.TIDE_BF16, shared_expert=s.shared_expert)
     seed = args.seed + 1000 * rank  # each rank runs its own blocks (weak scaling)
+    ep = args.ep
+    El = E // world if ep else E
+    if ep:
+        cap = min(args.capacity or El, El)
+        pool_mode = False
+        uid = [tide.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            torch.distributed.broadcast_object_list(uid, src=0)
 
     # weights: generated on the device (bit-identical to the host generator), packed by the
-    # product API (tide_pack_expert); one context per layer
+    # product API (tide_pack_expert); one context per layer (EP: this rank's E/P experts)
     layers = []
     for l in range(Lyr):
         wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev)
+        if ep:
+            sl = slice(rank * El, (rank + 1) * El)
+            wg, wu, wd = wg[sl].contiguous(), wu[sl].contiguous(), wd[sl].contiguous()
         packed = tide.pack_layer(desc, wg, wu, wd)
         del wg, wu, wd
+        torch.cuda.empty_cache()
         shared = torch.cat([a.reshape(-1) for a in sh]).contiguous() if sh else None
         w = {"device_all": packed} if not pool_mode else {"host_master": packed.cpu().pin_memory()}
         if pool_mode:
             del packed
-        layers.append(dict(router=wr, w=w, shared=shared,
-                           ctx=tide.Context(desc, cap, 16, local_rank),
+        if ep:
+            ctx = tide.EPContext(desc, uid[0] if l == 0 else None, rank, world, local_rank,
+                                 like=None if l == 0 else layers[0]["ctx"])
+        else:
+            ctx = tide.Context(desc, cap, 16, local_rank)
+        layers.append(dict(router=wr, w=w, shared=shared, ctx=ctx,
                            x=g.block_hidden_torch(s, seed, l, dev),
-                           pl=torch.zeros(E, dtype=torch.uint8, device=dev),
+                           pl=torch.zeros(El, dtype=torch.uint8, device=dev),
                            hits=torch.empty(E, dtype=torch.int32, device=dev),
                            out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
     torch.cuda.synchronize()
     T = s.steps
 
     def layer_step(L, t, x=None, stats=False):
-        return L["ctx"].moe_step(L["x"][t] if x is None else x, L["router"], **L["w"],
+        xx = L["x"][t] if x is None else x
+        if ep:
+            return L["ctx"].moe_step_ep(xx, L["router"], L["w"]["device_all"],
+                                        shared_w=L["shared"], placement=L["pl"], step=t,
+                                        interval=args.interval, capacity=cap, out=L["out"],
+                                        hit_counts=L["hits"], placement_out=L["pl"], stats=stats)
+        return L["ctx"].moe_step(xx, L["router"], **L["w"],
                                  shared_w=L["shared"], placement=L["pl"], step=t,
                                  interval=args.interval, out=L["out"], hit_counts=L["hits"],
                                  placement_out=L["pl"], stats=stats)
@@ -248,7 +272,12 @@ def run_tide(args, rank: int, world: int, local_rank: int):
             u = r.stats["unique_experts"] + (1 if s.shared_expert else 0)
             uniq += u
             w_read += r.stats["weight_bytes_read"]
-            ffn_bytes += u * s.expert_bytes + act_bytes
+            if ep:  # this rank's local experts over every rank's rows
+                pairs = r.stats["resident_pairs"] + r.stats["nonresident_pairs"]
+                rows = pairs + (N if s.shared_expert else 0)
+                ffn_bytes += u * s.expert_bytes + rows * (H * 2 + 2 * F * 2 + H * 4)
+            else:
+                ffn_bytes += u * s.expert_bytes + act_bytes
             copies += r.stats["copies"]
             h2d += r.stats["h2d_bytes"]
     ffn_ms = sum(p["ffn_ms"] for p in phases)
@@ -329,7 +358,9 @@ def run_tide(args, rank: int, world: int, local_rank: int):
            "config": {"workload": workload_str(s, cap, args.interval), "layers": Lyr,
                       "tokens_per_layer_step": N, "num_experts": E, "top_k": k, "hidden": H,
                       "ffn": F, "capacity": cap, "interval": args.interval,
-                      "parallelism": f"replicas x{world} (each rank its own blocks)",
+                      "parallelism": (f"expert parallel x{world} (E/P = {El} experts per rank, "
+                                      "NCCL all-gather dispatch + all-to-all combine)") if ep
+                      else f"replicas x{world} (each rank its own blocks)",
                       "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
                             "through the stack between reuses"},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -201,6 +201,11 @@ TIDE_API tide_status tide_ctx_create_ep(const tide_layer_desc* desc, int32_t dev
                                         const void* nccl_unique_id, int32_t rank, int32_t world,
                                         tide_ctx** out);
 
+/* Another layer's context on the same rank/device sharing `parent`'s communicator
+ * (parent must outlive it).  Not collective. */
+TIDE_API tide_status tide_ctx_create_ep_like(const tide_layer_desc* desc, tide_ctx* parent,
+                                             tide_ctx** out);
+
 /* local_experts: device, E/P packed experts of this rank (expert r*E/P + i at slot i).
  * shared_w: device packed shared expert (iff TIDE_SHARED_EXPERT).  Other arguments as
  * tide_moe_step.  Every rank must call it for the same layer/step (collectives). */
@@ -217,7 +222,10 @@ TIDE_API tide_status tide_moe_step_ep(tide_ctx* ctx, const void* block_hidden, i
  *  router/route/gather/ffn/combine: a1, a2-a5, a5 gather, a7+a9 (experts in HBM),
  *  a10; staged: from the end of the resident FFN to the start of the combine
  *  in host_master mode (H2D waits + a8 FFN over staged chunks).
- *  launches: kernels this context launched while timing was enabled.        */
+ *  launches: kernels this context launched while timing was enabled.
+ *  Under EP (tide_moe_step_ep) the fields hold: router_ms = route kernel,
+ *  route_ms = dispatch all-gather, gather_ms = local lists + placement, ffn_ms = FFN,
+ *  staged_ms = partial sums + all-to-all, combine_ms = rank-order sum + hits gather.  */
 typedef struct {
   double router_ms, route_ms, gather_ms, ffn_ms, staged_ms, combine_ms, total_ms;
   int64_t steps, launches, ffn_launches;

@@ -163,6 +163,7 @@ struct tide_ctx {
   bool ep = false;
   int rank = 0, world = 1, El = 0, e0 = 0, rows_all = 0;
   ncclComm_t comm = nullptr;
+  bool own_comm = false;
   void* x_all = nullptr;        // [P*maxN, H] all ranks' tokens
   int* topk_all = nullptr;      // [P*maxN, k]
   float* gates_all = nullptr;   // [P*maxN, k]
@@ -289,7 +290,7 @@ void tide_ctx_destroy(tide_ctx* c) {
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm && c->own_comm) ncclCommDestroy(c->comm);
   delete c;
 }
 
@@ -408,9 +409,10 @@ tide_status tide_nccl_unique_id(void* out) {
   return TIDE_OK;
 }
 
-tide_status tide_ctx_create_ep(const tide_layer_desc* d, int32_t device, const void* nccl_id,
-                               int32_t rank, int32_t world, tide_ctx** out) {
-  if (!out || !nccl_id) return fail(TIDE_EINVAL, "null argument");
+static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
+                                      const void* nccl_id, tide_ctx* parent, int32_t rank,
+                                      int32_t world, tide_ctx** out) {
+  if (!out) return fail(TIDE_EINVAL, "null argument");
   *out = nullptr;
   tide_status s = validate_desc(d);
   if (s != TIDE_OK) return s;
@@ -448,16 +450,32 @@ tide_status tide_ctx_create_ep(const tide_layer_desc* d, int32_t device, const v
     tide_ctx_destroy(c);
     return fail(TIDE_ECUDA, "%s", m.c_str());
   }
-  ncclUniqueId id;
-  memcpy(&id, nccl_id, sizeof(id));
-  ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
-  if (r != ncclSuccess) {
-    c->comm = nullptr;
-    tide_ctx_destroy(c);
-    return fail(TIDE_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  if (parent) {
+    c->comm = parent->comm;
+  } else {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      tide_ctx_destroy(c);
+      return fail(TIDE_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    c->own_comm = true;
   }
   *out = c;
   return TIDE_OK;
+}
+
+tide_status tide_ctx_create_ep(const tide_layer_desc* d, int32_t device, const void* nccl_id,
+                               int32_t rank, int32_t world, tide_ctx** out) {
+  if (!nccl_id) return fail(TIDE_EINVAL, "nccl_unique_id is null");
+  return ctx_create_ep_impl(d, device, nccl_id, nullptr, rank, world, out);
+}
+
+tide_status tide_ctx_create_ep_like(const tide_layer_desc* d, tide_ctx* parent, tide_ctx** out) {
+  if (!parent || !parent->ep) return fail(TIDE_EINVAL, "parent is not an expert-parallel context");
+  return ctx_create_ep_impl(d, parent->device, nullptr, parent, parent->rank, parent->world, out);
 }
 
 // Lazily set up host_master resources (slot pool, staging ring, pinned mirrors).
@@ -971,9 +989,16 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   int* cnt = c->cnt + c->parity * E;
   int* cnt_next = c->cnt + (c->parity ^ 1) * E;
   c->parity ^= 1;
+  tide_ctx::Rec rec{};
+  const int64_t launches0 = c->launches, ffn0 = c->ffn_launches;
+  if (c->timing) {
+    for (cudaEvent_t& e : rec.ev) e = take_event(c);
+    CU_TRY(cudaEventRecord(rec.ev[0], st));
+  }
   // a1..a3 on this rank's tokens
   s = launch_route(c, x, N, wr, cnt, cnt_next, nullptr, st);
   if (s != TIDE_OK) return s;
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
   if (N < maxN) CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
   // dispatch: every rank's tokens and routing to every rank (fixed counts, no host sync)
   const ncclDataType_t xt = c->bf16 ? ncclBfloat16 : ncclFloat32;
@@ -982,6 +1007,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   NC_TRY(ncclAllGather(c->topk, c->topk_all, (size_t)maxN * k, ncclInt32, c->comm, st));
   NC_TRY(ncclAllGather(c->gates, c->gates_all, (size_t)maxN * k, ncclFloat32, c->comm, st));
   NC_TRY(ncclGroupEnd());
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[2], st));
   // local experts' token lists over all rows; their counts are the global hits (R-18)
   CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
   tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El, c->cnt_l,
@@ -990,15 +1016,18 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   c->launches++;
   s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El);
   if (s != TIDE_OK) return s;
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[3], st));
   // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
   s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true);
   if (s != TIDE_OK) return s;
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
   // a10: per-source partial sums, all-to-all, rank-order sum
   CU_TRY(launch_pdl(tide_ep_partial_kernel, dim3(R, (H + 511) / 512), dim3(128), 0, st,
                     (const float*)c->y_perm, (const int*)c->topk_all, (const float*)c->gates_all,
                     (const int*)c->pslot_all, (const int*)c->off_l, c->partial, k, H, c->e0, El));
   c->launches++;
   NC_TRY(ncclAlltoAll(c->partial, c->recv, (size_t)maxN * H, ncclFloat32, c->comm, st));
+  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
   if (N > 0) {
     const dim3 grid(N, (H + 511) / 512);
     const int srow = shared ? R * k : -1;
@@ -1013,6 +1042,12 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     c->launches++;
   }
   NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
+  if (c->timing) {
+    CU_TRY(cudaEventRecord(rec.ev[6], st));
+    rec.launches = c->launches - launches0;
+    rec.ffn_launches = c->ffn_launches - ffn0;
+    c->pending.push_back(rec);
+  }
   if (stats) {
     RouteInfo local;
     std::vector<int> hl(El);

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EP
 EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert_elems",
             "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
             "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing", "tide_nccl_unique_id",
-            "tide_ctx_create_ep", "tide_moe_step_ep")
+            "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep")
 
 
 class TideError(RuntimeError):
@@ -102,6 +102,8 @@ def lib():
         L.tide_ctx_create_ep.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_int32, ctypes.c_void_p,
                                          ctypes.c_int32, ctypes.c_int32,
                                          ctypes.POINTER(ctypes.c_void_p)]
+        L.tide_ctx_create_ep_like.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_void_p,
+                                              ctypes.POINTER(ctypes.c_void_p)]
         L.tide_moe_step_ep.argtypes = [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
@@ -256,11 +258,15 @@ def nccl_unique_id() -> bytes:
 class EPContext(Context):
     """tide_ctx_create_ep: expert-parallel context (rank of world), own NCCL communicator."""
 
-    def __init__(self, desc: LayerDesc, unique_id: bytes, rank: int, world: int, device: int = 0):
+    def __init__(self, desc: LayerDesc, unique_id: bytes | None, rank: int, world: int,
+                 device: int = 0, like: "EPContext | None" = None):
         h = ctypes.c_void_p()
-        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-        _check(lib().tide_ctx_create_ep(ctypes.byref(desc), device, uid, rank, world,
-                                        ctypes.byref(h)))
+        if like is not None:  # share `like`'s NCCL communicator
+            _check(lib().tide_ctx_create_ep_like(ctypes.byref(desc), like.handle, ctypes.byref(h)))
+        else:
+            uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+            _check(lib().tide_ctx_create_ep(ctypes.byref(desc), device, uid, rank, world,
+                                            ctypes.byref(h)))
         self.handle = h
         self.desc = desc
         self.rank, self.world = rank, world
