@@ -134,6 +134,8 @@ typedef struct {
   float* logits;     /* [N, E] fp32 router logits                                 */
   uint64_t* route_trace; /* [4 * route CTAs] %globaltimer ns per route-kernel CTA:
                             start, phase 1 done, phase 2 start, phase 2 done (0 = n/a) */
+  uint64_t* ffn_trace;   /* [8 * #SMs] per FFN CTA: entry, work list ready, producer done,
+                            epilogue done (%globaltimer ns), items processed                */
 } tide_step_debug;
 
 typedef struct tide_ctx tide_ctx;

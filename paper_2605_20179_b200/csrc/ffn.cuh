@@ -57,6 +57,7 @@ struct FfnParams {
   void* h_out;
   float* y_out;
   int H, F, E, maxN, N, k, shared;
+  unsigned long long* trace;  // debug: per CTA [entry, work list ready, producer done, epilogue done, items]
   int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
   int shared_tok0;       // token id of its first row (0 single-device, rank*maxN under EP)
 };
@@ -90,6 +91,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   int4* s_ent = reinterpret_cast<int4*>(s_tok + kMaxTok);  // build mode: this CTA's work list
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* tr = p.trace ? p.trace + 8 * blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer_ns();
   const int H = p.H, F = p.F;
   const int FT = (F + kTileM - 1) / kTileM, HT = (H + kTileM - 1) / kTileM;
   const int KB1 = H / BK, KB2 = F / BK;
@@ -160,13 +163,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     } else {
       n_ent = *p.n_entries;
     }
-    if (lane == 0) {
+    // warp-wide producer: lane 0 schedules, waits and loads the weight tiles; lane i
+    // issues the i-th token-row load of each stage (gather4 / box), so large entries are
+    // not bound by a single thread's TMA issue rate
+    if (tr && lane == 0) tr[1] = globaltimer_ns();
+    int n_items = 0;
     const int n1 = n_ent * FT, total = n1 + n_ent * HT;
     const uint64_t pol_w = policy_evict_first(), pol_a = policy_evict_last();
     int stage = 0, islot = 0;
     uint32_t sphase = 0, iphase = 0;
     while (true) {
-      const int it = atomicAdd(p.sched, 1);
+      int it = 0;
+      if (lane == 0) it = atomicAdd(p.sched, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
       FfnItem item;
       item.kind = -1;
       if (it < total) {
@@ -178,70 +187,87 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         item.flags = en.z >> 16; item.tokbase = en.w;
         item.entry = entry;
       }
-      mbar_wait(&iempty[islot], iphase ^ 1);
-      items[islot] = item;
-      mbar_arrive(&ifull[islot]);
+      if (lane == 0) {
+        mbar_wait(&iempty[islot], iphase ^ 1);
+        items[islot] = item;
+        mbar_arrive(&ifull[islot]);
+      }
+      __syncwarp();
       if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
       if (item.kind < 0) break;
+      ++n_items;
       const int nbox = (item.m + 15) >> 4;
       if (item.kind == 0) {
-        // token rows of this entry, gathered straight from x_in (4 rows per gather4;
-        // rows past m repeat the last token -- their MMA columns are discarded)
+        // token rows of this entry, gathered straight from x_in: lane i loads rows
+        // 4i..4i+3 (rows past m repeat the last token; their MMA columns are discarded)
         const int ng = (item.m + 3) >> 2;
-        for (int j = 0; j < 4 * ng; ++j) {
-          const int jj = item.tokbase + min(j, item.m - 1);
-          s_tok[j] = (item.flags & 2) ? jj : __ldcg(p.list + jj);
+        int4 rows4 = make_int4(0, 0, 0, 0);
+        if (lane < ng) {
+          int rr[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int jj = item.tokbase + min(4 * lane + i, item.m - 1);
+            rr[i] = (item.flags & 2) ? jj : __ldcg(p.list + jj);
+          }
+          rows4 = make_int4(rr[0], rr[1], rr[2], rr[3]);
         }
         const CUtensorMap* ma = (item.flags & 1) ? &p.map_gu_s : &p.map_gu;
         const int rowg = item.slot * 3 * F + item.tile * kTileM;
         const int rowu = rowg + F;
         for (int kb = 0; kb < KB1; ++kb) {
-          mbar_wait(&empty[stage], sphase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + 2 * kATile;
-          mbar_arrive_expect_tx(&full[stage], 2 * kATile + ng * 512);
-          tma_load_2d(sa, ma, &full[stage], kb * BK, rowg, pol_w);
-          tma_load_2d(sa + kATile, ma, &full[stage], kb * BK, rowu, pol_w);
-          for (int gi = 0; gi < ng; ++gi)
-            tma_gather4(sb + gi * 512, &p.map_x, &full[stage], kb * BK,
-                        make_int4(s_tok[4 * gi], s_tok[4 * gi + 1], s_tok[4 * gi + 2], s_tok[4 * gi + 3]),
-                        pol_a);
+          if (lane == 0) {
+            mbar_wait(&empty[stage], sphase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], 2 * kATile + ng * 512);
+            tma_load_2d(sa, ma, &full[stage], kb * BK, rowg, pol_w);
+            tma_load_2d(sa + kATile, ma, &full[stage], kb * BK, rowu, pol_w);
+          }
+          __syncwarp();
+          if (lane < ng) tma_gather4(sb + lane * 512, &p.map_x, &full[stage], kb * BK, rows4, pol_a);
           if (++stage == kStages) { stage = 0; sphase ^= 1; }
         }
       } else {
         // h of this entry must be complete (all FT phase-1 tiles, possibly on other SMs)
-        const int* dp = p.done + item.entry;
-        if (ld_acquire_gpu(dp) < FT) {
-          const uint64_t t0 = globaltimer_ns();
-          while (ld_acquire_gpu(dp) < FT) {
-            __nanosleep(64);
-            if (globaltimer_ns() - t0 > 4000000000ull) {
-              printf("tide: ffn dependency watchdog entry %d\n", item.entry);
-              __trap();
+        if (lane == 0) {
+          const int* dp = p.done + item.entry;
+          if (ld_acquire_gpu(dp) < FT) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_gpu(dp) < FT) {
+              __nanosleep(64);
+              if (globaltimer_ns() - t0 > 4000000000ull) {
+                printf("tide: ffn dependency watchdog entry %d\n", item.entry);
+                __trap();
+              }
             }
           }
         }
+        __syncwarp();
         fence_proxy_async_global();
         const CUtensorMap* ma = (item.flags & 1) ? &p.map_d_s : &p.map_d;
         const int rowd = item.slot * 3 * H + 2 * H + item.tile * kTileM;
         const bool dual = item.m <= 64;
         for (int kb = 0; kb < KB2; kb += dual ? 2 : 1) {
           const int nk = (dual && kb + 1 < KB2) ? 2 : 1;
-          mbar_wait(&empty[stage], sphase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + 2 * kATile;
-          mbar_arrive_expect_tx(&full[stage], nk * (kATile + nbox * 2048));
-          for (int q = 0; q < nk; ++q) {
-            tma_load_2d(sa + q * kATile, ma, &full[stage], (kb + q) * BK, rowd, pol_w);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(sb + (q * nbox + b) * 2048, &p.map_h, &full[stage], (kb + q) * BK,
-                          item.off + 16 * b, pol_a);
+          if (lane == 0) {
+            mbar_wait(&empty[stage], sphase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], nk * (kATile + nbox * 2048));
+            for (int q = 0; q < nk; ++q)
+              tma_load_2d(sa + q * kATile, ma, &full[stage], (kb + q) * BK, rowd, pol_w);
+          }
+          __syncwarp();
+          if (lane < nk * nbox) {
+            const int q = lane / nbox, b = lane % nbox;
+            tma_load_2d(sb + (q * nbox + b) * 2048, &p.map_h, &full[stage], (kb + q) * BK,
+                        item.off + 16 * b, pol_a);
           }
           if (++stage == kStages) { stage = 0; sphase ^= 1; }
         }
       }
     }
-    }  // lane 0
+    if (tr && lane == 0) { tr[2] = globaltimer_ns(); tr[4] = n_items; }
   } else if (warp == 1 && lane == 0) {
     // ===================== MMA issuer (one thread) =====================
     int stage = 0, islot = 0, acc = 0;
@@ -353,6 +379,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       }
     }
   }
+  if (tr && threadIdx.x == 64) tr[3] = globaltimer_ns();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();

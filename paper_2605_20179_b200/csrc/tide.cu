@@ -514,7 +514,8 @@ static tide_status ensure_pool(tide_ctx* c) {
 // global mode: entries/n_entries (host-built staged chunk).
 static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
-                              int N, cudaStream_t st, bool ep_local = false) {
+                              int N, cudaStream_t st, bool ep_local = false,
+                              unsigned long long* trace = nullptr) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -539,6 +540,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.N = N;
   p.k = c->k;
   p.shared = (c->d.flags & TIDE_SHARED_EXPERT) ? 1 : 0;
+  p.trace = trace;
   p.shared_row0 = N * c->k;
   p.shared_tok0 = 0;
   if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
@@ -893,7 +895,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   // ---------------- a7/a9 FFN over the hit experts already in HBM (+ shared expert)
   if (N > 0) {
     s = launch_ffn(c, cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
-                   c->ffn_ctrl + 1, N, st);
+                   c->ffn_ctrl + 1, N, st, false,
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));

@@ -60,7 +60,7 @@ class StepStats(ctypes.Structure):
 
 class StepDebug(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("topk_idx", "gates", "pos", "order", "offsets",
-                                                "logits", "route_trace")]
+                                                "logits", "route_trace", "ffn_trace")]
 
 
 class PhaseTimes(ctypes.Structure):
@@ -226,7 +226,9 @@ class Context:
                      "offsets": torch.empty(E + 1, dtype=torch.int32, device=dev),
                      "logits": torch.empty(N, E, dtype=torch.float32, device=dev),
                      "route_trace": torch.zeros(4 * ((E + 7) // 8) * max(1, (N + 7) // 4),
-                                                dtype=torch.int64, device=dev)}
+                                                dtype=torch.int64, device=dev),
+                     "ffn_trace": torch.zeros(8 * torch.cuda.get_device_properties(dev).multi_processor_count,
+                                              dtype=torch.int64, device=dev)}
             dbg = StepDebug(*(dbg_t[n].data_ptr() for n, _ in StepDebug._fields_))
         _check(lib().tide_moe_step(
             self.handle, _ptr(block_hidden), N, _ptr(router_w), ctypes.byref(w), _ptr(placement),
