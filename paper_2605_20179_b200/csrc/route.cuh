@@ -27,28 +27,31 @@ constexpr int kRouterWarps = 8;     // experts per CTA in phase 1 (one per warp)
 constexpr int kMaxTok = 128;        // tokens per FFN work entry (MMA N <= 128)
 
 // ---------------------------------------------------------------- a1 helpers
+// Sum of the products of one 16-byte chunk, by a fixed pairwise tree in fp32.  bf16 x bf16
+// products are exact in fp32, so the only roundings are the tree's (3 levels for bf16).
+// Chunk sums are accumulated in fp64 by the caller (R-17: |logit - fp64| stays ~2e-7 even
+// when one feature dominates a lane's sum, e.g. the popularity-bias column).
 template <typename T>
-__device__ __forceinline__ float dot16B(uint4 xa, uint4 wa, float acc);
+__device__ __forceinline__ float chunk_dot(uint4 xa, uint4 wa);
 template <>
-__device__ __forceinline__ float dot16B<__nv_bfloat16>(uint4 xa, uint4 wa, float acc) {
+__device__ __forceinline__ float chunk_dot<__nv_bfloat16>(uint4 xa, uint4 wa) {
   const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa);
   const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wa);
+  float q[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 xf = __bfloat1622float2(x2[i]);
-    float2 wf = __bfloat1622float2(w2[i]);
-    acc = fmaf(xf.x, wf.x, acc);
-    acc = fmaf(xf.y, wf.y, acc);
+    const float2 xf = __bfloat1622float2(x2[i]);
+    const float2 wf = __bfloat1622float2(w2[i]);
+    q[i] = __fmul_rn(xf.x, wf.x) + __fmul_rn(xf.y, wf.y);
   }
-  return acc;
+  return (q[0] + q[1]) + (q[2] + q[3]);
 }
 template <>
-__device__ __forceinline__ float dot16B<float>(uint4 xa, uint4 wa, float acc) {
-  acc = fmaf(__uint_as_float(xa.x), __uint_as_float(wa.x), acc);
-  acc = fmaf(__uint_as_float(xa.y), __uint_as_float(wa.y), acc);
-  acc = fmaf(__uint_as_float(xa.z), __uint_as_float(wa.z), acc);
-  acc = fmaf(__uint_as_float(xa.w), __uint_as_float(wa.w), acc);
-  return acc;
+__device__ __forceinline__ float chunk_dot<float>(uint4 xa, uint4 wa) {
+  return fmaf(__uint_as_float(xa.x), __uint_as_float(wa.x),
+              __uint_as_float(xa.y) * __uint_as_float(wa.y)) +
+         fmaf(__uint_as_float(xa.z), __uint_as_float(wa.z),
+              __uint_as_float(xa.w) * __uint_as_float(wa.w));
 }
 
 // Info block written for the host (one D2H copy in host_master mode).
@@ -138,101 +141,21 @@ __device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 
   return total;
 }
 
-// grid (ceil(E/8), ceil(N/tpc)), 256 threads.  EPL = logits per lane in the top-k
-// (power of two >= E/32).
-template <typename T, int EPL>
-__global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_constant__ RouteParams p) {
-  __shared__ int s_flag;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int E = p.E, N = p.N, H = p.H, k = p.k;
-  const int NW = (N + 31) >> 5;
-  const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
-  pdl_wait();     // X may be written by the previous kernel in the stream
-  pdl_trigger();  // let the FFN grid start its prologue
-  unsigned long long* tr =
-      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
-  if (blockIdx.x == 0 && blockIdx.y == 0) {
-    for (int i = tid; i < E; i += blockDim.x) p.cnt_next[i] = 0;
-    for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
-  }
-
-  // ================= phase 1: router logits (a1)
+// a2 + a3 for token n by one warp.  v_in[i] = logit of expert lane + 32 i.
+// Lane l sorts its logits by (value desc, id asc) in registers, then k rounds of a warp
+// argmax over the lanes' heads (the winner pops); gates (R-2); per-expert counts, token
+// lists and bitmasks by atomics.
+template <int EPL>
+__device__ __forceinline__ void route_token(const RouteParams& p, int n, const float (&v_in)[EPL]) {
+  const int lane = threadIdx.x & 31;
+  const int E = p.E, k = p.k, NW = (p.N + 31) >> 5;
   {
-    constexpr int G = 8;  // 16-byte chunks in flight per lane per group
-    const int e = blockIdx.x * kRouterWarps + warp;
-    const int chunks = H * (int)sizeof(T) / 16;
-    const bool copy_x = blockIdx.x == 0 && warp == 0;
-    if (e < E) {
-      const uint4* wrow = reinterpret_cast<const uint4*>(static_cast<const T*>(p.wr) + (size_t)e * H);
-      for (int n = n0; n < n1; n += 2) {
-        const bool two = n + 1 < n1;
-        const uint4* x0 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)n * H);
-        const uint4* x1 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)(two ? n + 1 : n) * H);
-        uint4* y0 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)n * H);
-        uint4* y1 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)(two ? n + 1 : n) * H);
-        float a0 = 0.f, a1 = 0.f;
-        for (int base = 0; base < chunks; base += 32 * G) {
-          uint4 wv[G], xv0[G], xv1[G];
-#pragma unroll
-          for (int i = 0; i < G; ++i) {
-            const int c = base + lane + 32 * i;
-            if (c < chunks) {
-              wv[i] = __ldg(wrow + c);
-              xv0[i] = __ldg(x0 + c);
-              xv1[i] = __ldg(x1 + c);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < G; ++i) {
-            const int c = base + lane + 32 * i;
-            if (c < chunks) {
-              a0 = dot16B<T>(xv0[i], wv[i], a0);
-              a1 = dot16B<T>(xv1[i], wv[i], a1);
-              if (copy_x) {
-                y0[c] = xv0[i];
-                y1[c] = xv1[i];
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        }
-        if (lane == 0) {
-          p.logits[(size_t)n * E + e] = a0;
-          if (two) p.logits[(size_t)(n + 1) * E + e] = a1;
-        }
-      }
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    if (tr) tr[1] = globaltimer_ns();
-    __threadfence();
-    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-  if (tid == 0) {
-    p.g_cnt[blockIdx.y] = 0;
-    if (tr) tr[2] = globaltimer_ns();
-  }
-
-  // ================= phase 2: top-k of this token group (a2) + histogram (a3)
-  // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
-  // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
-  for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
     float v[EPL];
     int id[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
       const int e = lane + 32 * i;
-      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+      v[i] = e < E ? v_in[i] : -INFINITY;
       id[i] = e;
     }
 #pragma unroll
@@ -287,6 +210,104 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
       p.pair_slot[(size_t)n * k + lane] = slot;
       atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
     }
+    }
+}
+
+// grid (ceil(E/8), ceil(N/tpc)), 256 threads.  EPL = logits per lane in the top-k
+// (power of two >= E/32).
+template <typename T, int EPL>
+__global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = p.E, N = p.N, H = p.H;
+  const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
+  pdl_wait();     // X may be written by the previous kernel in the stream
+  pdl_trigger();  // let the FFN grid start its prologue
+  unsigned long long* tr =
+      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int i = tid; i < E; i += blockDim.x) p.cnt_next[i] = 0;
+    for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
+  }
+
+  // ================= phase 1: router logits (a1)
+  {
+    constexpr int G = 8;  // 16-byte chunks in flight per lane per group
+    const int e = blockIdx.x * kRouterWarps + warp;
+    const int chunks = H * (int)sizeof(T) / 16;
+    const bool copy_x = blockIdx.x == 0 && warp == 0;
+    if (e < E) {
+      const uint4* wrow = reinterpret_cast<const uint4*>(static_cast<const T*>(p.wr) + (size_t)e * H);
+      for (int n = n0; n < n1; n += 2) {
+        const bool two = n + 1 < n1;
+        const uint4* x0 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)n * H);
+        const uint4* x1 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)(two ? n + 1 : n) * H);
+        uint4* y0 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)n * H);
+        uint4* y1 = reinterpret_cast<uint4*>(static_cast<T*>(p.x_in) + (size_t)(two ? n + 1 : n) * H);
+        double a0 = 0.0, a1 = 0.0;
+        for (int base = 0; base < chunks; base += 32 * G) {
+          uint4 wv[G], xv0[G], xv1[G];
+#pragma unroll
+          for (int i = 0; i < G; ++i) {
+            const int c = base + lane + 32 * i;
+            if (c < chunks) {
+              wv[i] = __ldg(wrow + c);
+              xv0[i] = __ldg(x0 + c);
+              xv1[i] = __ldg(x1 + c);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < G; ++i) {
+            const int c = base + lane + 32 * i;
+            if (c < chunks) {
+              a0 += (double)chunk_dot<T>(xv0[i], wv[i]);
+              a1 += (double)chunk_dot<T>(xv1[i], wv[i]);
+              if (copy_x) {
+                y0[c] = xv0[i];
+                y1[c] = xv1[i];
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if (lane == 0) {
+          p.logits[(size_t)n * E + e] = (float)a0;
+          if (two) p.logits[(size_t)(n + 1) * E + e] = (float)a1;
+        }
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    if (tr) tr[1] = globaltimer_ns();
+    __threadfence();
+    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  if (tid == 0) {
+    p.g_cnt[blockIdx.y] = 0;
+    if (tr) tr[2] = globaltimer_ns();
+  }
+
+  // ================= phase 2: top-k of this token group (a2) + histogram (a3)
+  // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
+  // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
+  for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
+    float v[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+    }
+    route_token<EPL>(p, n, v);
   }
   if (tr) {
     __syncthreads();

@@ -251,3 +251,25 @@ def test_device_generator_matches_host_bits():
     h = g.expert_np(g.MINI, 7, 3, 17)
     for a, b in zip((wg, wu, wd), h):
         assert (g.torch_to_np(a) == b).all()
+
+
+@pytest.mark.parametrize("shape_name,tokens", [("mini", 32), ("mini", 256), ("flash", 32),
+                                               ("flash", 200)])
+def test_router_logit_error(shape_name, tokens):
+    """R-17: the GPU's fp32 logits stay within 6e-7 of the fp64 oracle, so a routing flip
+    needs an fp64 logit gap below ~1e-6 (which the near-tie flag covers)."""
+    shape = g.SHAPES[shape_name]
+    E, H = shape.num_experts, shape.hidden
+    wr = g.router_np(shape, 51, 0)
+    x = g.block_hidden_np(shape, 51, steps=1, tokens=tokens)[0]
+    ref = oracle.router_logits(x, wr)
+    sh = g.Shape(shape.name, E, shape.top_k, H, 64, 1, tokens, dtype="bf16")  # router only
+    layer = DeviceLayer(sh, 51)
+    from paper_2605_20179_b200 import tide
+    ctx = tide.Context(desc_for(sh, max_tokens=tokens), E)
+    r = ctx.moe_step(g.np_to_torch(x, "cuda"), g.np_to_torch(wr, "cuda"), **layer.weights(),
+                     placement=torch.zeros(E, dtype=torch.uint8, device="cuda"), step=0,
+                     interval=1, debug=True)
+    torch.cuda.synchronize()
+    err = np.abs(r.debug["logits"].cpu().numpy().astype(np.float64) - ref).max()
+    assert err < 6e-7, f"max |logit - fp64| = {err:.3e}"
