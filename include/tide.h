@@ -65,7 +65,14 @@ typedef enum { TIDE_F32 = 0, TIDE_BF16 = 1 } tide_dtype;
 enum {
   TIDE_NORM_TOPK = 1u << 0,     /* renormalise the k selected gates (R-2)          */
   TIDE_SHARED_EXPERT = 1u << 1, /* add one always-resident shared expert (R-16)    */
-  TIDE_LAZY_PROMOTE = 1u << 2   /* copy a promoted expert on its first hit (R-9)   */
+  TIDE_LAZY_PROMOTE = 1u << 2,  /* copy a promoted expert on its first hit (R-9)   */
+  /* NEXT-1 hit-counter readings (default: the current step's hits, R-5).  With one of
+   * these, a refresh ranks experts by hits accumulated over earlier steps of the block
+   * (no lookahead): WINDOW = since the previous refresh, reset at each refresh (SPEC
+   * S:242); CUMULATIVE = since the block's step 0.  Step 0 ranks by its own hits. */
+  TIDE_COUNTER_WINDOW = 1u << 3,
+  TIDE_COUNTER_CUMULATIVE = 1u << 4,
+  TIDE_TIE_INCUMBENT = 1u << 5  /* equal counts: experts already resident rank first */
 };
 
 /* Shape of one MoE layer.  Constraints checked by tide_ctx_create:
@@ -234,6 +241,35 @@ typedef struct {
 } tide_phase_times;
 TIDE_API tide_status tide_ctx_set_timing(tide_ctx* ctx, int32_t enable);
 TIDE_API tide_status tide_ctx_get_timing(tide_ctx* ctx, tide_phase_times* out);
+
+/* ------------------------------------------------------------------------
+ * NEXT-2: refresh-interval model (Eq. 4-7), host-only.
+ *   io(tau)   = c_io * (B*T/tau) * (1 - (1-d)^tau)                      (Eq. 5)
+ *   miss(tau) = c_miss * T * B * f(tau), f(tau) = (1/tau) sum_{j<tau} (1-(1-d)^j)
+ *                                                                        (Eq. 6)
+ *   tau* = argmin over tau in [1, T-1] of io + miss, ties -> smallest     (Eq. 7)
+ * d: drift rate (Eq. 4, e.g. from tide_trace_stats); c_io: cost of one expert
+ * migration; c_miss: cost of one stale resident slot per step (on B200 the miss
+ * is an H2D stream of the expert, R-13, so c_miss ~ c_io).  curve: [T-1] or NULL.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t T, B;
+  double d, c_io, c_miss;
+} tide_interval_model;
+TIDE_API tide_status tide_interval_cost(const tide_interval_model* m, int32_t tau,
+                                        double* io_cost, double* miss_cost);
+TIDE_API tide_status tide_optimize_interval(const tide_interval_model* m, int32_t* tau_out,
+                                            double* curve);
+
+/* NEXT-4: routing-trace analytics on the device.
+ *  counts : device [T][E] int32 per-step hit counts (e.g. hit_counts of T steps)
+ *  sim    : device [T][T] fp64 cosine similarity of the count vectors (0 if a vector is 0)
+ *  unique : device [T] experts with hits > 0 per step
+ *  drift  : device [T-1] Eq. 4 drift of the top-B placement between consecutive steps
+ * Enqueued on `stream`; 1 <= B <= E <= 4096. */
+TIDE_API tide_status tide_trace_stats(const int32_t* counts, int32_t T, int32_t E, int32_t B,
+                                      double* sim, int32_t* unique, double* drift,
+                                      void* stream);
 
 /* Thread-local description of the last failure on this thread. */
 TIDE_API const char* tide_last_error(void);

@@ -267,3 +267,86 @@ def ep_step(L: Layer, P: int, x: np.ndarray, k: int, placement_in: np.ndarray, s
                            interval, capacity_per_rank, _p(topk_idx), _p(h), _p(pout), _p(out))
     assert rc == 0
     return topk_idx, h, pout, out
+
+
+# ---------------------------------------------------------------- NEXT-2 / NEXT-4
+def _d(fn):
+    f = getattr(lib(), fn)
+    f.restype = ctypes.c_double
+    return f
+
+
+def migration_cost(tau, B, T, d, c_io=1.0):
+    f = _d("orc_migration_cost")
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double]
+    return f(tau, B, T, d, c_io)
+
+
+def miss_fraction(tau, d):
+    f = _d("orc_miss_fraction")
+    f.argtypes = [ctypes.c_int, ctypes.c_double]
+    return f(tau, d)
+
+
+def miss_cost(tau, B, T, d, c_miss=1.0):
+    f = _d("orc_miss_cost")
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double]
+    return f(tau, B, T, d, c_miss)
+
+
+def optimize_tau(T, B, d, c_io, c_miss):
+    curve = np.zeros(max(1, T - 1), np.float64)
+    f = lib().orc_optimize_tau
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                  ctypes.c_void_p]
+    tau = f(T, B, d, c_io, c_miss, _p(curve))
+    return tau, curve
+
+
+def cosine(a, b):
+    a = np.ascontiguousarray(a, np.int32)
+    b = np.ascontiguousarray(b, np.int32)
+    f = _d("orc_cosine")
+    f.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    return f(a.shape[0], _p(a), _p(b))
+
+
+def unique(hits_):
+    h = np.ascontiguousarray(hits_, np.int32)
+    return lib().orc_unique(h.shape[0], _p(h))
+
+
+def drift(prev, cur, B):
+    a = np.ascontiguousarray(prev, np.int32)
+    b = np.ascontiguousarray(cur, np.int32)
+    f = _d("orc_drift")
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    return f(a.shape[0], B, _p(a), _p(b))
+
+
+# ---------------------------------------------------------------- NEXT-1
+COUNTER_CURRENT, COUNTER_WINDOW, COUNTER_CUMULATIVE = 0, 1, 2
+
+
+def counter_key(mode, step, hits_, acc):
+    h = np.ascontiguousarray(hits_, np.int32)
+    a = np.ascontiguousarray(acc, np.int32)
+    out = np.empty_like(h)
+    lib().orc_counter_key(h.shape[0], mode, step, _p(h), _p(a), _p(out))
+    return out
+
+
+def counter_update(mode, step, refresh, hits_, acc):
+    """Updates ``acc`` (int32, contiguous) in place."""
+    h = np.ascontiguousarray(hits_, np.int32)
+    assert acc.dtype == np.int32 and acc.flags.c_contiguous
+    lib().orc_counter_update(h.shape[0], mode, step, int(refresh), _p(h), _p(acc))
+
+
+def placement_ex(key, capacity, refresh, incumbent_ties, placement_in):
+    k_ = np.ascontiguousarray(key, np.int32)
+    pin = np.ascontiguousarray(placement_in, np.uint8)
+    out = np.empty(k_.shape[0], np.uint8)
+    assert lib().orc_placement_ex(k_.shape[0], capacity, _p(k_), int(refresh), int(incumbent_ties),
+                                  _p(pin), _p(out)) == 0
+    return out

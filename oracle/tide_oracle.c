@@ -319,3 +319,111 @@ int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
   free(y);
   return 0;
 }
+
+/* ---------------- NEXT-2: Eq. 5 --------------------------------------- */
+double orc_migration_cost(int tau, int B, int T, double d, double c_io) {
+  return c_io * ((double)B * (double)T / (double)tau) * (1.0 - pow(1.0 - d, (double)tau));
+}
+
+/* f(tau): mean fraction of the placement made stale by drift over an interval,
+ * (1/tau) sum_{j=0}^{tau-1} (1 - (1-d)^j)  (Eq. 6 is stated only as monotone). */
+double orc_miss_fraction(int tau, double d) {
+  double s = 0.0;
+  for (int j = 0; j < tau; ++j) s += 1.0 - pow(1.0 - d, (double)j);
+  return s / (double)tau;
+}
+
+/* Eq. 6 with the miss cost of this build (R-13). */
+double orc_miss_cost(int tau, int B, int T, double d, double c_miss) {
+  return c_miss * (double)T * (double)B * orc_miss_fraction(tau, d);
+}
+
+/* Eq. 7: exhaustive scan of tau in [1, T-1] ("greedy search");
+ * curve[tau-1] = total cost; ties -> smallest tau. */
+int orc_optimize_tau(int T, int B, double d, double c_io, double c_miss, double* curve) {
+  int best = 1;
+  double best_c = 0.0;
+  for (int tau = 1; tau <= (T > 1 ? T - 1 : 1); ++tau) {
+    double c = orc_migration_cost(tau, B, T, d, c_io) + orc_miss_cost(tau, B, T, d, c_miss);
+    if (curve) curve[tau - 1] = c;
+    if (tau == 1 || c < best_c) {
+      best = tau;
+      best_c = c;
+    }
+  }
+  return best;
+}
+
+/* ---------------- NEXT-4: cosine similarity of count vectors ----------- */
+double orc_cosine(int E, const int32_t* a, const int32_t* b) {
+  double ab = 0.0, aa = 0.0, bb = 0.0;
+  for (int e = 0; e < E; ++e) {
+    ab += (double)a[e] * (double)b[e];
+    aa += (double)a[e] * (double)a[e];
+    bb += (double)b[e] * (double)b[e];
+  }
+  if (aa == 0.0 || bb == 0.0) return 0.0;
+  return ab / (sqrt(aa) * sqrt(bb));
+}
+
+int orc_unique(int E, const int32_t* hits) {
+  int u = 0;
+  for (int e = 0; e < E; ++e) u += hits[e] > 0;
+  return u;
+}
+
+/* Eq. 4: drift of the optimal (top-B) placement between two steps. */
+double orc_drift(int E, int B, const int32_t* prev, const int32_t* cur) {
+  uint8_t* a = (uint8_t*)malloc((size_t)E);
+  uint8_t* b = (uint8_t*)malloc((size_t)E);
+  orc_placement(E, B, prev, 1, a, a);
+  orc_placement(E, B, cur, 1, b, b);
+  int diff = 0;
+  for (int e = 0; e < E; ++e) diff += (b[e] && !a[e]);
+  free(a);
+  free(b);
+  return (double)diff / (double)B;
+}
+
+/* ---------------- NEXT-1: counters ("counts accumulated over [t_prev_refresh, t)",
+ * reset at refresh; S:269 cumulative variant; S:270 current-step "oracle mode" = R-5) -- */
+void orc_counter_key(int E, int mode, int step, const int32_t* hits, const int32_t* acc,
+                     int32_t* key) {
+  for (int e = 0; e < E; ++e) key[e] = (mode == 0 || step == 0) ? hits[e] : acc[e];
+}
+
+void orc_counter_update(int E, int mode, int step, int refresh, const int32_t* hits,
+                        int32_t* acc) {
+  if (mode == 0) return;
+  for (int e = 0; e < E; ++e) {
+    if (step == 0 || (mode == 1 && refresh)) acc[e] = 0;
+    acc[e] += hits[e];
+  }
+}
+
+/* Top-C with the incumbent-aware tie-break: among equal keys, experts
+ * already in the input placement rank first, then lower id. */
+int orc_placement_ex(int E, int capacity, const int32_t* key, int refresh, int incumbent_ties,
+                     const uint8_t* placement_in, uint8_t* placement_out) {
+  if (capacity < 1 || capacity > E) return 1;
+  if (!refresh) {
+    for (int e = 0; e < E; ++e) placement_out[e] = placement_in[e] ? 1 : 0;
+    return 0;
+  }
+  for (int e = 0; e < E; ++e) {
+    int rank = 0;
+    for (int f = 0; f < E; ++f) {
+      int before;
+      if (key[f] != key[e]) {
+        before = key[f] > key[e];
+      } else if (incumbent_ties && ((placement_in[f] != 0) != (placement_in[e] != 0))) {
+        before = placement_in[f] != 0;
+      } else {
+        before = f < e;
+      }
+      rank += before;
+    }
+    placement_out[e] = rank < capacity ? 1 : 0;
+  }
+  return 0;
+}

@@ -107,6 +107,40 @@ int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
                 const uint8_t* placement_in, int step, int interval, int capacity_per_rank,
                 int32_t* topk_idx, int32_t* hits, uint8_t* placement_out, double* out);
 
+/* ---------------- NEXT-1: hit-counter readings ("global hit counter"; S:242,
+ * S:269-270) and the incumbent-aware tie-break.
+ * mode 0 = current step (R-5); 1 = window [t_prev_refresh, t) reset at each refresh
+ * (SPEC default); 2 = cumulative since block start.  In modes 1/2 step 0 of a block
+ * ranks by its own hits (SPEC OracleStep0 cold start) and acc restarts.
+ * orc_counter_key: the counts that rank experts at this step.
+ * orc_counter_update: acc after the step (reset at refresh in mode 1, then += hits).
+ * orc_placement_ex: top-C by (key desc, [incumbent first], id asc).             */
+void orc_counter_key(int E, int mode, int step, const int32_t* hits, const int32_t* acc,
+                     int32_t* key);
+void orc_counter_update(int E, int mode, int step, int refresh, const int32_t* hits,
+                        int32_t* acc);
+int orc_placement_ex(int E, int capacity, const int32_t* key, int refresh, int incumbent_ties,
+                     const uint8_t* placement_in, uint8_t* placement_out);
+
+/* ---------------- NEXT-2: refresh-interval model (Eq. 4-7) ----------
+ * Eq. 5: Lat_IO(tau) = c_io * (B*T/tau) * (1 - (1-d)^tau).
+ * Eq. 6: Lat_miss(tau) = c_miss * T * B * f(tau), f(tau) = (1/tau) * sum_{j<tau} (1-(1-d)^j)
+ *        (SPEC S:330's closed form of the paper's monotone f).  On B200 a miss streams
+ *        the expert H2D (R-13), so c_miss is a per-expert H2D cost, not a CPU cost.
+ * Eq. 7: tau* = argmin_{1 <= tau <= T-1} Lat_IO + Lat_miss (ties -> smallest tau). */
+double orc_migration_cost(int tau, int B, int T, double d, double c_io);
+double orc_miss_fraction(int tau, double d);
+double orc_miss_cost(int tau, int B, int T, double d, double c_miss);
+int orc_optimize_tau(int T, int B, double d, double c_io, double c_miss, double* curve);
+
+/* ---------------- NEXT-4: routing-trace analytics -- */
+/* cosine similarity of two hit-count vectors (0 if either is all-zero).            */
+double orc_cosine(int E, const int32_t* a, const int32_t* b);
+/* experts with hits > 0                                                            */
+int orc_unique(int E, const int32_t* hits);
+/* Eq. 4: d = |topB(cur) \ topB(prev)| / B, top-B by (hits desc, id asc).           */
+double orc_drift(int E, int B, const int32_t* prev, const int32_t* cur);
+
 #ifdef __cplusplus
 }
 #endif

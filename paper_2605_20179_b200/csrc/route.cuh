@@ -91,6 +91,9 @@ struct BookParams {
   const int* topk_idx;  // [N,k]
   const uint8_t* placement_in;
   int N, E, k, refresh, capacity;
+  int* acc;             // [E] NEXT-1 counter state (ctx-owned)
+  int mode;             // 0 current step (R-5), 1 window since last refresh, 2 cumulative
+  int step, incumbent;  // block-relative step; incumbent-aware ties
   int* hit_counts;      // [E] caller buffer
   uint8_t* placement_out;  // [E] caller buffer
   int* order;           // [E]
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
 }
 
 // One CTA (1024 threads): a4 placement and a5 bookkeeping from the hit counts.
-// dynamic smem: 5 * E ints.
+// dynamic smem: 6 * E ints.
 __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__ BookParams p) {
   extern __shared__ int book_smem[];
   __shared__ int s_scratch[33];
@@ -329,10 +332,15 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
   int* s_order = s_pl + E;
   int* s_bstart = s_order + E;
   int* s_tmp = s_bstart + E;
+  int* s_key = s_tmp + E;  // the counts that rank experts at this step (NEXT-1)
   if (tid == 0) { s_cnt = 0; s_prom = 0; s_evic = 0; s_rp = 0; s_uq = 0; }
-  for (int e = tid; e < E; e += blockDim.x) s_hits[e] = __ldcg(p.cnt + e);
+  for (int e = tid; e < E; e += blockDim.x) {
+    s_hits[e] = __ldcg(p.cnt + e);
+    s_key[e] = (p.mode == 0 || p.step == 0) ? s_hits[e] : p.acc[e];
+    s_pl[e] = p.placement_in[e] != 0;  // incumbents (overwritten below)
+  }
   __syncthreads();
-  if (p.refresh) {  // rank(e) = #{f : hits[f] > hits[e] or (== and f < e)}
+  if (p.refresh) {  // rank(e) = #{f : key[f] > key[e] or (== and [incumbent f] or f < e)}
     const int S = max(1, (int)blockDim.x / E);   // threads per expert
     const int seg = (E + S - 1) / S;
     for (int e = tid; e < E; e += blockDim.x) s_tmp[e] = 0;
@@ -340,22 +348,22 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
     for (int idx = tid; idx < E * S; idx += blockDim.x) {
       const int e = idx % E, sg = idx / E;
       const int f0 = sg * seg, f1 = min(E, f0 + seg);
-      const int he = s_hits[e];
+      const int he = s_key[e];
+      const int ie = p.incumbent ? s_pl[e] : 0;
       int r = 0;
 #pragma unroll 8
       for (int f = f0; f < f1; ++f) {
-        const int hf = s_hits[f];
-        r += (hf > he) || (hf == he && f < e);
+        const int hf = s_key[f];
+        const int jf = p.incumbent ? s_pl[f] : 0;
+        r += (hf > he) || (hf == he && (jf > ie || (jf == ie && f < e)));
       }
       atomicAdd(&s_tmp[e], r);
     }
     __syncthreads();
     for (int e = tid; e < E; e += blockDim.x) s_pl[e] = s_tmp[e] < p.capacity;
   } else {
-    for (int e = tid; e < E; e += blockDim.x) {
-      s_pl[e] = p.placement_in[e] != 0;
+    for (int e = tid; e < E; e += blockDim.x)
       if (s_pl[e]) atomicAdd(&s_cnt, 1);
-    }
   }
   __syncthreads();
   int* info_hits = reinterpret_cast<int*>(p.info + 1);
@@ -369,6 +377,9 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
     if (tid == 0) p.info->status = 3;
     return;
   }
+  if (p.mode != 0)  // NEXT-1 counter state after this step
+    for (int e = tid; e < E; e += blockDim.x)
+      p.acc[e] = ((p.step == 0 || (p.mode == 1 && p.refresh)) ? 0 : p.acc[e]) + s_hits[e];
   for (int e = tid; e < E; e += blockDim.x) {
     const int was = p.placement_in[e] != 0, res = s_pl[e];
     if (res && !was) atomicAdd(&s_prom, 1);

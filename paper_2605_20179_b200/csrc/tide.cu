@@ -28,6 +28,7 @@
 #include <nccl.h>
 
 #include "../../include/tide.h"
+#include "analytics.cuh"
 #include "ep.cuh"
 #include "ffn.cuh"
 #include "route.cuh"
@@ -134,6 +135,7 @@ struct tide_ctx {
   RouteInfo* info = nullptr; // + hits[E] + placement[E]
   size_t info_bytes = 0;
   int* slot_of_dev = nullptr;
+  int* counter_acc = nullptr;  // [E] NEXT-1 counter state
 
   // host_master mode
   void* pool = nullptr;            // (capacity + staging) packed experts
@@ -275,7 +277,7 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv};
+                 c->partial, c->recv, c->counter_acc};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -363,6 +365,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->info_bytes = sizeof(RouteInfo) + sizeof(int) * E + E;
   ALLOC(c->info, c->info_bytes);
   ALLOC(c->slot_of_dev, sizeof(int) * E);
+  ALLOC(c->counter_acc, sizeof(int) * E);
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_route, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_book, cudaEventDisableTiming) != cudaSuccess ||
@@ -385,7 +388,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
     cudaFuncSetAttribute(tide_ffn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kFfnSmemBytes);
   cudaFuncSetAttribute(tide_book_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(sizeof(int) * 5 * E));
+                       (int)(sizeof(int) * 6 * E));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     tide_ctx_destroy(c);
@@ -600,7 +603,8 @@ static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, 
 
 static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
                                int refresh, int capacity, int32_t* hit_counts,
-                               uint8_t* placement_out, cudaStream_t st, int E_override = 0) {
+                               uint8_t* placement_out, cudaStream_t st, int E_override = 0,
+                               int step = 0) {
   const int E = E_override ? E_override : c->E;
   BookParams b;
   b.cnt = cnt;
@@ -613,13 +617,17 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   b.k = c->k;
   b.refresh = refresh;
   b.capacity = capacity;
+  b.acc = c->counter_acc;
+  b.mode = (c->d.flags & TIDE_COUNTER_WINDOW) ? 1 : (c->d.flags & TIDE_COUNTER_CUMULATIVE) ? 2 : 0;
+  b.step = step;
+  b.incumbent = (c->d.flags & TIDE_TIE_INCUMBENT) ? 1 : 0;
   b.hit_counts = hit_counts;
   b.placement_out = placement_out;
   b.order = c->order;
   b.offsets = c->offsets;
   b.pos = c->pos;
   b.info = c->info;
-  tide_book_kernel<<<1, 1024, sizeof(int) * 5 * E, st>>>(b);
+  tide_book_kernel<<<1, 1024, sizeof(int) * 6 * E, st>>>(b);
   CU_TRY(cudaGetLastError());
   c->launches++;
   return TIDE_OK;
@@ -877,14 +885,15 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
 
   // ---------------- a4/a5 bookkeeping (placement, buckets, pos, info)
   if (pool_mode) {
-    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, st);
+    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, st, 0, step);
     if (s != TIDE_OK) return s;
     CU_TRY(cudaMemcpyAsync(c->h_info, c->info, c->info_bytes, cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaEventRecord(c->ev_info, st));
   } else {
     CU_TRY(cudaEventRecord(c->ev_route, st));
     CU_TRY(cudaStreamWaitEvent(c->side, c->ev_route, 0));
-    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, c->side);
+    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, c->side, 0,
+                    step);
     if (s != TIDE_OK) return s;
     CU_TRY(cudaEventRecord(c->ev_book, c->side));
   }
@@ -1017,7 +1026,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
                                                           c->list_l, R, c->pslot_all);
   CU_TRY(cudaGetLastError());
   c->launches++;
-  s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El);
+  s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El,
+                  step);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[3], st));
   // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
@@ -1068,6 +1078,58 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     for (int e = 0; e < El; ++e) stats->nonresident_pairs += hl[e];
     stats->nonresident_pairs -= local.resident_pairs;
   }
+  return TIDE_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-2 (host)
+tide_status tide_interval_cost(const tide_interval_model* m, int32_t tau, double* io_cost,
+                               double* miss_cost) {
+  if (!m || !io_cost || !miss_cost) return fail(TIDE_EINVAL, "null argument");
+  if (tau < 1 || m->B < 1 || m->T < 1 || m->d < 0.0 || m->d > 1.0)
+    return fail(TIDE_EINVAL, "tau %d / B %d / T %d / d %g out of range", tau, m->B, m->T, m->d);
+  // Eq. 5: c_io * (B*T/tau) * (1 - (1-d)^tau)
+  double keep = 1.0;
+  for (int j = 0; j < tau; ++j) keep *= 1.0 - m->d;
+  *io_cost = m->c_io * ((double)m->B * m->T / tau) * (1.0 - keep);
+  // Eq. 6: c_miss * T * B * f(tau), f = mean stale fraction (1/tau) sum_{j<tau} (1-(1-d)^j)
+  double f = 0.0, kj = 1.0;
+  for (int j = 0; j < tau; ++j) {
+    f += 1.0 - kj;
+    kj *= 1.0 - m->d;
+  }
+  *miss_cost = m->c_miss * (double)m->T * m->B * (f / tau);
+  return TIDE_OK;
+}
+
+tide_status tide_optimize_interval(const tide_interval_model* m, int32_t* tau_out, double* curve) {
+  if (!m || !tau_out) return fail(TIDE_EINVAL, "null argument");
+  if (m->T < 2) return fail(TIDE_EINVAL, "T %d < 2", m->T);
+  int best = 1;
+  double best_c = 0.0;
+  for (int tau = 1; tau <= m->T - 1; ++tau) {  // Eq. 7 domain, exhaustive
+    double io, ms;
+    tide_status s = tide_interval_cost(m, tau, &io, &ms);
+    if (s != TIDE_OK) return s;
+    if (curve) curve[tau - 1] = io + ms;
+    if (tau == 1 || io + ms < best_c) {
+      best = tau;
+      best_c = io + ms;
+    }
+  }
+  *tau_out = best;
+  return TIDE_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-4 (device)
+tide_status tide_trace_stats(const int32_t* counts, int32_t T, int32_t E, int32_t B, double* sim,
+                             int32_t* unique, double* drift, void* stream) {
+  if (!counts || !sim || !unique || !drift) return fail(TIDE_EINVAL, "null argument");
+  if (T < 1 || E < 1 || E > 4096 || B < 1 || B > E) return fail(TIDE_EINVAL, "bad T/E/B");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  tide_trace_sim_kernel<<<dim3(T, T), 256, 0, st>>>(counts, T, E, sim);
+  CU_TRY(cudaGetLastError());
+  tide_trace_step_kernel<<<T, 1024, 2 * E, st>>>(counts, T, E, B, unique, drift);
+  CU_TRY(cudaGetLastError());
   return TIDE_OK;
 }
 

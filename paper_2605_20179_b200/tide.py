@@ -20,6 +20,7 @@ TIDE_OK, TIDE_EINVAL, TIDE_ECAPACITY, TIDE_EPLACEMENT, TIDE_ECUDA, TIDE_ENCCL, T
     TIDE_EUNSUPPORTED = range(8)
 TIDE_F32, TIDE_BF16 = 0, 1
 TIDE_NORM_TOPK, TIDE_SHARED_EXPERT, TIDE_LAZY_PROMOTE = 1, 2, 4
+TIDE_COUNTER_WINDOW, TIDE_COUNTER_CUMULATIVE, TIDE_TIE_INCUMBENT = 8, 16, 32
 
 STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EPLACEMENT",
                 4: "TIDE_ECUDA", 5: "TIDE_ENCCL", 6: "TIDE_ENOMEM", 7: "TIDE_EUNSUPPORTED"}
@@ -27,7 +28,8 @@ STATUS_NAMES = {0: "TIDE_OK", 1: "TIDE_EINVAL", 2: "TIDE_ECAPACITY", 3: "TIDE_EP
 EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert_elems",
             "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
             "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing", "tide_nccl_unique_id",
-            "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep")
+            "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep",
+            "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats")
 
 
 class TideError(RuntimeError):
@@ -72,6 +74,11 @@ class PhaseTimes(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class IntervalModel(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int32), ("B", ctypes.c_int32), ("d", ctypes.c_double),
+                ("c_io", ctypes.c_double), ("c_miss", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -109,6 +116,14 @@ def lib():
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(StepStats),
             ctypes.c_void_p]
+        L.tide_interval_cost.argtypes = [ctypes.POINTER(IntervalModel), ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
+        L.tide_optimize_interval.argtypes = [ctypes.POINTER(IntervalModel),
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]
+        L.tide_trace_stats.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p]
         L.tide_ctx_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.tide_ctx_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(PhaseTimes)]
         _lib = L
@@ -134,9 +149,14 @@ def torch_dtype(code: int):
 
 
 def make_desc(num_experts, top_k, hidden, ffn, max_tokens, dtype=TIDE_BF16,
-              norm_topk=True, shared_expert=False, lazy_promote=False) -> LayerDesc:
+              norm_topk=True, shared_expert=False, lazy_promote=False, counter="current",
+              incumbent_ties=False) -> LayerDesc:
+    """counter: "current" (R-5), "window" or "cumulative" (NEXT-1)."""
     flags = (TIDE_NORM_TOPK if norm_topk else 0) | (TIDE_SHARED_EXPERT if shared_expert else 0) \
-        | (TIDE_LAZY_PROMOTE if lazy_promote else 0)
+        | (TIDE_LAZY_PROMOTE if lazy_promote else 0) \
+        | {"current": 0, "window": TIDE_COUNTER_WINDOW,
+           "cumulative": TIDE_COUNTER_CUMULATIVE}[counter] \
+        | (TIDE_TIE_INCUMBENT if incumbent_ties else 0)
     return LayerDesc(num_experts, top_k, hidden, ffn, max_tokens, dtype, flags)
 
 
@@ -299,3 +319,34 @@ class EPContext(Context):
             _ptr(placement_out), ctypes.byref(st) if st is not None else None,
             _stream_ptr(stream)))
         return StepOutputs(out, hit_counts, placement_out, st.as_dict() if st else None, None)
+
+
+def interval_cost(T: int, B: int, d: float, c_io: float, c_miss: float, tau: int):
+    """tide_interval_cost -> (Eq. 5 I/O cost, Eq. 6 miss cost)."""
+    m = IntervalModel(T, B, d, c_io, c_miss)
+    io, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().tide_interval_cost(ctypes.byref(m), tau, ctypes.byref(io), ctypes.byref(ms)))
+    return io.value, ms.value
+
+
+def optimize_interval(T: int, B: int, d: float, c_io: float, c_miss: float):
+    """tide_optimize_interval -> (tau*, [total cost for tau = 1..T-1])."""
+    import numpy as np
+    m = IntervalModel(T, B, d, c_io, c_miss)
+    tau = ctypes.c_int32()
+    curve = np.zeros(max(1, T - 1), np.float64)
+    _check(lib().tide_optimize_interval(ctypes.byref(m), ctypes.byref(tau),
+                                        ctypes.c_void_p(curve.ctypes.data)))
+    return tau.value, curve
+
+
+def trace_stats(counts, B: int, stream=None):
+    """tide_trace_stats on a device [T, E] int32 tensor -> (sim [T,T] f64, unique [T], drift [T-1])."""
+    T, E = counts.shape
+    dev = counts.device
+    sim = torch.empty(T, T, dtype=torch.float64, device=dev)
+    uniq = torch.empty(T, dtype=torch.int32, device=dev)
+    drift = torch.empty(max(1, T - 1), dtype=torch.float64, device=dev)
+    _check(lib().tide_trace_stats(_ptr(counts.contiguous()), T, E, B, _ptr(sim), _ptr(uniq),
+                                  _ptr(drift), _stream_ptr(stream)))
+    return sim, uniq, drift[: T - 1]
