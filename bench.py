@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--graph", action="store_true",
+                    help="NEXT-3: replay one CUDA graph per block step t (all layers) in the timed region")
     ap.add_argument("--ep", action="store_true",
                     help="expert parallelism over the ranks (tide_moe_step_ep) instead of replicas")
     return ap.parse_args()
@@ -215,14 +217,32 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                                  interval=args.interval, out=L["out"], hit_counts=L["hits"],
                                  placement_out=L["pl"], stats=stats)
 
-    def bench_step(i):
+    graphs = None
+
+    def bench_step(i, eager=False):
         t = i % T
+        if graphs is not None and not eager:
+            graphs[t].replay()
+            return
         for L in layers:
             layer_step(L, t)
 
     for i in range(args.warmup):
         bench_step(i)
     torch.cuda.synchronize()
+    if args.graph:  # NEXT-3: one graph per block step t, every layer-step of the stack in it
+        gl = []
+        for t in range(T):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for L in layers:
+                    layer_step(L, t)
+            gl.append(gr)
+        torch.cuda.synchronize()
+        graphs = gl
+        for i in range(args.warmup):  # placement state continues from the eager warm-up
+            bench_step(args.warmup + i)
+        torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
@@ -234,7 +254,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         e0.record(st)
         for i in range(args.steps):
-            bench_step(args.warmup + i)
+            bench_step(args.warmup + i, eager=phase_timing)
         e1.record(st)
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1)
@@ -298,16 +318,18 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
         "fallback 6.65 TB/s (B200_PROFILING.md)"
     achieved = per_launch_bytes / ffn_avg_s / 1e9
-    traffic = None
+    traffic, traffic_detail = None, None
     tp = os.path.join(ROOT, "profiles", "ffn_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(s.name)
+            traffic_detail = json.load(open(tp)).get(s.name)
+            traffic = traffic_detail["dram_bytes_per_launch"] if traffic_detail else None
         except Exception:
-            traffic = None
+            traffic, traffic_detail = None, None
     flops_per_layer_step = 2 * N * k * 3 * H * F + (2 * N * 3 * H * F if s.shared_expert else 0)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_detail": traffic_detail,
                 "kernel": "tide_ffn_kernel (grouped SwiGLU, tcgen05 + TMA)",
                 "peak_source": peak_src,
                 "bytes_per_launch": round(per_launch_bytes),
@@ -362,7 +384,9 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                                       "NCCL all-gather dispatch + all-to-all combine)") if ep
                       else f"replicas x{world} (each rank its own blocks)",
                       "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
-                            "through the stack between reuses"},
+                            "through the stack between reuses",
+                      "launch": ("CUDA graph per block step (all layers), replayed" if graphs
+                                 else "eager stream (PDL-chained kernels)")},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
            "gpu_launches": launches * world if rank == 0 else launches,
            "clocks": clocks,

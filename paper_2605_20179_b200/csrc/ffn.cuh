@@ -46,7 +46,8 @@ struct FfnParams {
   // build mode (cnt != nullptr): every CTA builds the list from the per-expert counts:
   // experts in id order with m > 0 and (slot_of == nullptr or slot_of[e] >= 0), rows
   // off[e] = prefix of counts in id order, then the shared expert (rows N*k + n).
-  const int* cnt;        // [E] per-expert token counts (build mode)
+  const int* cnt;        // [E] per-expert token counts (build mode), or [2][E] with par
+  const int* par;        // nullable: route's parity word, this step's counts = cnt[par^1]
   const int* slot_of;    // [E] pool slot (nullptr: slot = e)
   int* off_out;          // [E] row offsets written by CTA 0 (build mode; read by combine)
   const int4* entries;   // global mode: host-built list
@@ -126,10 +127,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     const int4* ents = p.entries;
     if (p.cnt) {  // build this CTA's copy of the work list (warp 0, expert ranges per lane)
       const int E = p.E;
+      const int* cnt = p.par ? p.cnt + (__ldcg(p.par) ^ 1) * E : p.cnt;
       const int per = (E + 31) >> 5, e0 = min(E, lane * per), e1 = min(E, e0 + per);
       int rows = 0, nent = 0;
       for (int e = e0; e < e1; ++e) {
-        const int m = __ldcg(p.cnt + e);
+        const int m = __ldcg(cnt + e);
         const bool in_hbm = !p.slot_of || __ldcg(p.slot_of + e) >= 0;
         rows += m;
         nent += (m > 0 && in_hbm) ? (m + kMaxTok - 1) / kMaxTok : 0;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       }
       int row = rows_x - rows, ei = ent_x - nent;
       for (int e = e0; e < e1; ++e) {
-        const int m = __ldcg(p.cnt + e);
+        const int m = __ldcg(cnt + e);
         const int slot = p.slot_of ? __ldcg(p.slot_of + e) : e;
         if (blockIdx.x == 0) p.off_out[e] = row;
         if (m > 0 && slot >= 0)

@@ -74,8 +74,11 @@ struct RouteParams {
   int* topk_idx;        // [N,k]
   float* gates;         // [N,k]
   int* pair_slot;       // [N,k] slot of pair (n,j) in its expert's token list
-  int* cnt;             // [E] this step's per-expert token counts (zero on entry)
-  int* cnt_next;        // [E] the other parity buffer: zeroed here for the next step
+  int* cnt2;            // [2][E] per-expert token counts, double-buffered: this step counts
+                        // into cnt2[par] (zero on entry) and zeroes cnt2[par^1] for the next
+  int* par;             // device parity word, flipped by the last CTA (so any stream-ordered
+                        // or graph-replayed sequence of steps stays consistent)
+  int* g_done;          // completion counter of the phase-2 CTAs (self-resetting)
   int* list;            // [E * maxN] tokens of each expert (arrival order)
   unsigned* mask;       // [E * NW] token bitmasks (zeroed by tide_book_kernel)
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
@@ -85,7 +88,8 @@ struct RouteParams {
 };
 
 struct BookParams {
-  const int* cnt;       // [E] hits
+  const int* cnt;       // [E] hits, or [2][E] selected by par (see RouteParams)
+  const int* par;       // nullable: cnt is double-buffered, this step's half = par^1
   const unsigned* mask; // [E * NW]
   unsigned* mask_rw;    // same, zeroed after use
   const int* topk_idx;  // [N,k]
@@ -149,7 +153,8 @@ __device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 
 // argmax over the lanes' heads (the winner pops); gates (R-2); per-expert counts, token
 // lists and bitmasks by atomics.
 template <int EPL>
-__device__ __forceinline__ void route_token(const RouteParams& p, int n, const float (&v_in)[EPL]) {
+__device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int n,
+                                            const float (&v_in)[EPL]) {
   const int lane = threadIdx.x & 31;
   const int E = p.E, k = p.k, NW = (p.N + 31) >> 5;
   {
@@ -208,7 +213,7 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int n, const f
     if (lane < k) {
       p.topk_idx[(size_t)n * k + lane] = my_e;
       p.gates[(size_t)n * k + lane] = expf(my_l - m) / denom;
-      const int slot = atomicAdd(&p.cnt[my_e], 1);
+      const int slot = atomicAdd(&cnt[my_e], 1);
       p.list[(size_t)my_e * p.maxN + slot] = n;
       p.pair_slot[(size_t)n * k + lane] = slot;
       atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
@@ -229,8 +234,10 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   unsigned long long* tr =
       p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
+  const int par = __ldcg(p.par);  // read before this CTA arrives: the flip comes after all arrive
+  int* cnt = p.cnt2 + par * E;
   if (blockIdx.x == 0 && blockIdx.y == 0) {
-    for (int i = tid; i < E; i += blockDim.x) p.cnt_next[i] = 0;
+    for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
   }
 
@@ -310,11 +317,17 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
       const int e = lane + 32 * i;
       v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
     }
-    route_token<EPL>(p, n, v);
+    route_token<EPL>(p, cnt, n, v);
   }
-  if (tr) {
-    __syncthreads();
-    if (tid == 0) tr[3] = globaltimer_ns();
+  __syncthreads();
+  if (tid == 0) {
+    if (tr) tr[3] = globaltimer_ns();
+    __threadfence();
+    if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
+      *p.g_done = 0;
+      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
+      __threadfence();
+    }
   }
 }
 
@@ -334,8 +347,9 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
   int* s_tmp = s_bstart + E;
   int* s_key = s_tmp + E;  // the counts that rank experts at this step (NEXT-1)
   if (tid == 0) { s_cnt = 0; s_prom = 0; s_evic = 0; s_rp = 0; s_uq = 0; }
+  const int* cnt = p.par ? p.cnt + (__ldcg(p.par) ^ 1) * E : p.cnt;
   for (int e = tid; e < E; e += blockDim.x) {
-    s_hits[e] = __ldcg(p.cnt + e);
+    s_hits[e] = __ldcg(cnt + e);
     s_key[e] = (p.mode == 0 || p.step == 0) ? s_hits[e] : p.acc[e];
     s_pl[e] = p.placement_in[e] != 0;  // incumbents (overwritten below)
   }

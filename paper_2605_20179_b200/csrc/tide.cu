@@ -113,14 +113,14 @@ struct tide_ctx {
   bool bf16 = true;
   size_t eb = 2, expert_elems = 0, expert_bytes = 0;
   int max_rows = 0, max_entries = 0;
-  int parity = 0;  // which of the two count buffers this step uses
 
   // workspaces (device)
   float* logits = nullptr;
   int* topk = nullptr;
   float* gates = nullptr;
   int* pair_slot = nullptr;
-  int* cnt = nullptr;        // [2][E] per-expert token counts (double-buffered by step parity)
+  int* cnt = nullptr;        // [2][E] per-expert token counts (double-buffered, see cnt_par)
+  int* cnt_par = nullptr;    // [2] device parity word + route completion counter
   int* list = nullptr;       // [E * maxN] per-expert token lists
   unsigned* mask = nullptr;  // [E * NWmax] per-expert token bitmasks
   int* g_cnt = nullptr;      // [maxN + 2] route-kernel last-CTA counters
@@ -277,7 +277,7 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv, c->counter_acc};
+                 c->partial, c->recv, c->counter_acc, c->cnt_par};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -351,6 +351,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->gates, sizeof(float) * N * k);
   ALLOC(c->pair_slot, sizeof(int) * N * k);
   ALLOC(c->cnt, sizeof(int) * 2 * E);
+  ALLOC(c->cnt_par, sizeof(int) * 2);
   ALLOC(c->list, sizeof(int) * (size_t)E * N);
   ALLOC(c->mask, sizeof(unsigned) * E * c->NWmax);
   ALLOC(c->g_cnt, sizeof(int) * (N + 2));
@@ -518,7 +519,7 @@ static tide_status ensure_pool(tide_ctx* c) {
 static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
                               int N, cudaStream_t st, bool ep_local = false,
-                              unsigned long long* trace = nullptr) {
+                              unsigned long long* trace = nullptr, const int* par = nullptr) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -527,6 +528,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.map_x = c->map_x;
   p.map_h = c->map_h;
   p.cnt = cnt;
+  p.par = par;
   p.slot_of = slot_of;
   p.off_out = c->off;
   p.entries = entries;
@@ -604,10 +606,11 @@ static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, 
 static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
                                int refresh, int capacity, int32_t* hit_counts,
                                uint8_t* placement_out, cudaStream_t st, int E_override = 0,
-                               int step = 0) {
+                               int step = 0, const int* par = nullptr) {
   const int E = E_override ? E_override : c->E;
   BookParams b;
   b.cnt = cnt;
+  b.par = par;
   b.mask = c->mask;
   b.mask_rw = c->mask;
   b.topk_idx = c->topk;
@@ -633,8 +636,8 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   return TIDE_OK;
 }
 
-static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* wr, int* cnt,
-                                int* cnt_next, tide_step_debug* dbg, cudaStream_t st) {
+static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* wr,
+                                tide_step_debug* dbg, cudaStream_t st) {
   const int E = c->E, k = c->k, H = c->H;
   RouteParams rp;
   rp.x = x;
@@ -651,8 +654,9 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.topk_idx = c->topk;
   rp.gates = c->gates;
   rp.pair_slot = c->pair_slot;
-  rp.cnt = cnt;
-  rp.cnt_next = cnt_next;
+  rp.cnt2 = c->cnt;
+  rp.par = c->cnt_par;
+  rp.g_done = c->cnt_par + 1;
   rp.list = c->list;
   rp.mask = c->mask;
   rp.g_cnt = c->g_cnt;
@@ -868,9 +872,6 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
                                      pool_mode ? c->capacity + c->staging : E,
                                      shared ? w->shared_w : nullptr);
   if (s != TIDE_OK) return s;
-  int* cnt = c->cnt + c->parity * E;
-  int* cnt_next = c->cnt + (c->parity ^ 1) * E;
-  c->parity ^= 1;
 
   tide_ctx::Rec rec{};
   const int64_t launches0 = c->launches, ffn0 = c->ffn_launches;
@@ -879,21 +880,22 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     CU_TRY(cudaEventRecord(rec.ev[0], st));
   }
   // ---------------- a1..a3: router, top-k, hits and per-expert token lists
-  s = launch_route(c, x, N, wr, cnt, cnt_next, dbg, st);
+  s = launch_route(c, x, N, wr, dbg, st);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
 
   // ---------------- a4/a5 bookkeeping (placement, buckets, pos, info)
   if (pool_mode) {
-    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, st, 0, step);
+    s = launch_book(c, c->cnt, placement, N, refresh, capacity, hit_counts, placement_out, st, 0,
+                    step, c->cnt_par);
     if (s != TIDE_OK) return s;
     CU_TRY(cudaMemcpyAsync(c->h_info, c->info, c->info_bytes, cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaEventRecord(c->ev_info, st));
   } else {
     CU_TRY(cudaEventRecord(c->ev_route, st));
     CU_TRY(cudaStreamWaitEvent(c->side, c->ev_route, 0));
-    s = launch_book(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out, c->side, 0,
-                    step);
+    s = launch_book(c, c->cnt, placement, N, refresh, capacity, hit_counts, placement_out, c->side, 0,
+                    step, c->cnt_par);
     if (s != TIDE_OK) return s;
     CU_TRY(cudaEventRecord(c->ev_book, c->side));
   }
@@ -903,9 +905,9 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   }
   // ---------------- a7/a9 FFN over the hit experts already in HBM (+ shared expert)
   if (N > 0) {
-    s = launch_ffn(c, cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
+    s = launch_ffn(c, c->cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
                    c->ffn_ctrl + 1, N, st, false,
-                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr);
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
@@ -998,9 +1000,6 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   const int refresh = (step % interval) == 0;
   tide_status s = ensure_weight_maps(c, local_experts, El, shared ? shared_w : nullptr);
   if (s != TIDE_OK) return s;
-  int* cnt = c->cnt + c->parity * E;
-  int* cnt_next = c->cnt + (c->parity ^ 1) * E;
-  c->parity ^= 1;
   tide_ctx::Rec rec{};
   const int64_t launches0 = c->launches, ffn0 = c->ffn_launches;
   if (c->timing) {
@@ -1008,7 +1007,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     CU_TRY(cudaEventRecord(rec.ev[0], st));
   }
   // a1..a3 on this rank's tokens
-  s = launch_route(c, x, N, wr, cnt, cnt_next, nullptr, st);
+  s = launch_route(c, x, N, wr, nullptr, st);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
   if (N < maxN) CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
