@@ -109,6 +109,15 @@ struct BookParams {
 __device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
   return va > vb || (va == vb && ia < ib);
 }
+// Order-preserving uint32 key of a float (-0 folded into +0, so key order == float order,
+// equal floats <=> equal keys): the warp argmax below runs on redux.sync.
+__device__ __forceinline__ unsigned order_key(float v) {
+  const unsigned u = __float_as_uint(v + 0.0f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_value(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 
 // In-place exclusive scan of a[0..n) in shared memory by the whole CTA; returns the total.
 __device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 ints*/) {
@@ -187,14 +196,12 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
     int my_e = 0;
     float my_l = 0.f;
     for (int j = 0; j < k; ++j) {
-      float bv = v[0];
-      int bi = id[0];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
-      }
+      // warp argmax of the lane heads by (value desc, id asc): max key, then min id among
+      // the lanes holding it (two redux.sync instead of a 5-step shuffle butterfly)
+      const unsigned hk = order_key(v[0]);
+      const unsigned mk = __reduce_max_sync(0xffffffffu, hk);
+      const int bi = (int)__reduce_min_sync(0xffffffffu, hk == mk ? (unsigned)id[0] : 0xffffffffu);
+      const float bv = key_value(mk);
       if ((bi & 31) == lane) {
 #pragma unroll
         for (int i = 0; i + 1 < EPL; ++i) { v[i] = v[i + 1]; id[i] = id[i + 1]; }
@@ -454,9 +461,11 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            const int* __restrict__ pair_slot,
                                                            const int* __restrict__ off,
                                                            T* __restrict__ out, int N, int k,
-                                                           int H, int shared) {
+                                                           int H, int shared,
+                                                           unsigned long long* trace) {
   pdl_wait();
   pdl_trigger();
+  if (trace && threadIdx.x == 0) atomicMax(trace, globaltimer_ns());  // debug: latest start
   const int n = blockIdx.x, lane = threadIdx.x & 31;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
   // lane j < k fetches pair j's row and gate (one round of independent loads), then the
@@ -499,6 +508,7 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
   } else {
     *reinterpret_cast<float4*>(o) = acc;
   }
+  if (trace && threadIdx.x == 0) atomicMax(trace + 1, globaltimer_ns());  // debug: latest end
 }
 
 }  // namespace tide

@@ -648,7 +648,8 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.E = E;
   rp.H = H;
   rp.k = k;
-  rp.tpc = N <= 64 ? 4 : 8;
+  rp.tpc = N <= 64 ? 4 : 8;  // tokens per CTA row of the route grid
+  if (const char* e = getenv("TIDE_ROUTE_TPC")) rp.tpc = std::max(1, std::min(8, atoi(e)));  // tuning
   rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
   rp.maxN = c->maxN;
   rp.topk_idx = c->topk;
@@ -930,16 +931,18 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   // ---------------- a10 combine
   if (N > 0) {
     const dim3 grid(N, (H + 511) / 512);
+    unsigned long long* ctr =  // debug: [6] latest start, [7] latest end in CTA 0's FFN record
+        (dbg && dbg->ffn_trace) ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) + 6 : nullptr;
     if (c->bf16)
       CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->off,
-                        static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0));
+                        static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr));
     else
       CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), 0, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->off, static_cast<float*>(out),
-                        N, k, H, shared ? 1 : 0));
+                        N, k, H, shared ? 1 : 0, ctr));
     c->launches++;
   }
   if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4/a5 outputs

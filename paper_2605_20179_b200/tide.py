@@ -218,7 +218,7 @@ class Context:
     def moe_step(self, block_hidden, router_w, *, device_all=None, host_master=None,
                  shared_w=None, placement, step: int, interval: int, capacity: int | None = None,
                  out=None, hit_counts=None, placement_out=None, stats: bool = False,
-                 debug: bool = False, stream=None) -> StepOutputs:
+                 debug: bool | str = False, stream=None) -> StepOutputs:
         """tide_moe_step.  Tensors: block_hidden [N,H] (device), router_w [E,H] (device),
         device_all [E, 3HF] device or host_master [E, 3HF] pinned host, shared_w [3HF]
         device, placement [E] uint8 device."""
@@ -245,11 +245,14 @@ class Context:
                      "order": torch.empty(E, dtype=torch.int32, device=dev),
                      "offsets": torch.empty(E + 1, dtype=torch.int32, device=dev),
                      "logits": torch.empty(N, E, dtype=torch.float32, device=dev),
-                     "route_trace": torch.zeros(4 * ((E + 7) // 8) * max(1, (N + 7) // 4),
+                     "route_trace": torch.zeros(4 * ((E + 7) // 8) * max(1, N),
                                                 dtype=torch.int64, device=dev),
                      "ffn_trace": torch.zeros(8 * torch.cuda.get_device_properties(dev).multi_processor_count,
                                               dtype=torch.int64, device=dev)}
-            dbg = StepDebug(*(dbg_t[n].data_ptr() for n, _ in StepDebug._fields_))
+            if debug == "trace":  # kernel timestamps only: no extra copies on the stream
+                dbg_t = {n: (v if n.endswith("_trace") else None) for n, v in dbg_t.items()}
+            dbg = StepDebug(*((dbg_t[n].data_ptr() if dbg_t[n] is not None else None)
+                              for n, _ in StepDebug._fields_))
         _check(lib().tide_moe_step(
             self.handle, _ptr(block_hidden), N, _ptr(router_w), ctypes.byref(w), _ptr(placement),
             step, interval, self.capacity if capacity is None else capacity, _ptr(out),

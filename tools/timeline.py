@@ -31,9 +31,9 @@ for t in range(T_AT + 1):
     for L in layers:
         res.append(L["ctx"].moe_step(L["x"][t], L["wr"], device_all=L["w"], shared_w=L["sh"],
                                      placement=L["pl"], step=t, interval=4, placement_out=L["pl"],
-                                     debug=(t == T_AT)))
+                                     debug=("trace" if t == T_AT else False)))
 torch.cuda.synchronize()
-tpc = 4 if N <= 64 else 8
+tpc = int(os.environ.get("TIDE_ROUTE_TPC", 4 if N <= 64 else 8))
 ny = max(1, (N + tpc - 1) // tpc)
 rows = []
 for li, r in enumerate(res):
@@ -43,15 +43,20 @@ for li, r in enumerate(res):
     last = rt[rt[:, 2] > 0]
     rows.append(dict(r0=rt[:, 0].min(), r1=rt[:, 1].max(), r2s=last[:, 2].min(), r2=last[:, 3].max(),
                      f0=ft[:, 0].min(), fl=ft[:, 1].min(), flx=ft[:, 1].max(), fp=ft[:, 2].max(),
-                     fe=ft[:, 3].max(), fe_med=np.median(ft[:, 3])))
+                     fe=ft[:, 3].max(), fe_med=np.median(ft[:, 3]), fw=ft[:, 5].min(),
+                     fwx=ft[:, 5].max(), r0x=rt[:, 0].max(), c0=ft[0, 6], c1=ft[0, 7],
+                     p1med=np.median(rt[:, 1] - rt[:, 0]), p2med=np.median(last[:, 3] - last[:, 2])))
 t0 = rows[1]["r0"]
 us = lambda v: (v - t0) / 1e3  # noqa: E731
 print(f"{shape.name} t={T_AT}: times in us relative to layer 1's route start")
 for li in range(1, NL):
     R = rows[li]
     print(f" layer {li}: route {us(R['r0']):7.2f} .. p1 end {us(R['r1']):7.2f} .. p2 {us(R['r2s']):7.2f}-{us(R['r2']):7.2f} | "
-          f"ffn entry {us(R['f0']):7.2f} list {us(R['fl']):7.2f}/{us(R['flx']):7.2f} prod-done {us(R['fp']):7.2f} "
+          f"ffn entry {us(R['f0']):7.2f} pdl-wait done {us(R['fw']):7.2f}/{us(R['fwx']):7.2f} list {us(R['fl']):7.2f}/{us(R['flx']):7.2f} prod-done {us(R['fp']):7.2f} "
           f"epi med {us(R['fe_med']):7.2f} max {us(R['fe']):7.2f}")
+    print(f"   combine start (latest) {us(R['c0']):7.2f} end (latest) {us(R['c1']):7.2f}")
+    print(f"   route CTA start spread {(R['r0x'] - R['r0']) / 1e3:5.2f}  per-CTA phase1 median {R['p1med'] / 1e3:5.2f}"
+          f"  phase2 median {R['p2med'] / 1e3:5.2f}")
     if li + 1 < NL:
         print(f"   gap ffn end -> next route start {us(rows[li + 1]['r0']) - us(R['fe']):6.2f} us "
               f"(combine + launch)")
