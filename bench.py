@@ -56,8 +56,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--graph", action="store_true",
-                    help="NEXT-3: replay one CUDA graph per block step t (all layers) in the timed region")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every layer-step from the host in the timed region (default: "
+                         "NEXT-3 CUDA graphs, one per block step t covering all layers)")
+    ap.add_argument("--prefetch-mb", type=float, default=-1,
+                    help="NEXT-3 cross-layer L2 prefetch budget per layer-step (MB); "
+                         "-1 = default (32 MB when all experts are in HBM), 0 = off")
     ap.add_argument("--ep", action="store_true",
                     help="expert parallelism over the ranks (tide_moe_step_ep) instead of replicas")
     return ap.parse_args()
@@ -204,6 +208,13 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                            out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
     torch.cuda.synchronize()
     T = s.steps
+    # NEXT-3: each layer prefetches the next layer's likely experts into L2 (ring: the
+    # last layer prefetches layer 0 for the next step)
+    pf_mb = args.prefetch_mb if args.prefetch_mb >= 0 else (32.0 if not pool_mode and not ep else 0.0)
+    if pf_mb > 0 and not pool_mode and not ep:
+        for li, L in enumerate(layers):
+            nx = layers[(li + 1) % Lyr]
+            L["ctx"].set_prefetch(nx["ctx"], nx["w"]["device_all"], int(pf_mb * 1e6))
 
     def layer_step(L, t, x=None, stats=False):
         xx = L["x"][t] if x is None else x
@@ -230,7 +241,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     for i in range(args.warmup):
         bench_step(i)
     torch.cuda.synchronize()
-    if args.graph:  # NEXT-3: one graph per block step t, every layer-step of the stack in it
+    if not args.eager and not pool_mode and not ep:  # NEXT-3: one graph per block step t, every layer-step of the stack in it
         gl = []
         for t in range(T):
             gr = torch.cuda.CUDAGraph()
@@ -273,6 +284,23 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     clocks = clk.stop()
     # region 2: same steps with per-phase CUDA events on the launching stream (roofline)
     ms_phased, phases = timed_region(True)
+    # region 3: each step timed alone (events between steps): refresh vs skipped steps
+    # (SURVEY 8(d) metric 1; a step is a refresh step iff t % interval == 0)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        evs[i][0].record(st)
+        bench_step(args.warmup + i)
+        evs[i][1].record(st)
+    torch.cuda.synchronize()
+    per = [(a.elapsed_time(b), (args.warmup + i) % T % args.interval == 0)
+           for i, (a, b) in enumerate(evs)]
+    ref_ms = [m for m, r in per if r]
+    skp_ms = [m for m, r in per if not r]
+    step_split = {"ms_refresh_step": round(sum(ref_ms) / max(1, len(ref_ms)), 4),
+                  "ms_skipped_step": round(sum(skp_ms) / max(1, len(skp_ms)), 4),
+                  "refresh_steps": len(ref_ms), "skipped_steps": len(skp_ms)}
     layer_steps = args.steps * Lyr
     value = N * layer_steps * world / (ms / 1e3)
 
@@ -386,12 +414,14 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                       "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
                             "through the stack between reuses",
                       "launch": ("CUDA graph per block step (all layers), replayed" if graphs
-                                 else "eager stream (PDL-chained kernels)")},
+                                 else "eager stream (PDL-chained kernels)"),
+                      "prefetch_mb": pf_mb},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
            "gpu_launches": launches * world if rank == 0 else launches,
            "clocks": clocks,
            "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()},
            "ms_per_step_with_phase_events": round(ms_phased / args.steps, 4),
+           "step_split": step_split,
            "io": {"copies": copies, "h2d_bytes": h2d} if pool_mode else None}
     return res
 

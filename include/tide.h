@@ -243,6 +243,24 @@ TIDE_API tide_status tide_ctx_set_timing(tide_ctx* ctx, int32_t enable);
 TIDE_API tide_status tide_ctx_get_timing(tide_ctx* ctx, tide_phase_times* out);
 
 /* ------------------------------------------------------------------------
+ * NEXT-3: cross-layer L2 prefetch (P:278-281's "overlap" intent).
+ * After this call, every device_all tide_moe_step on `ctx` ends its FFN by prefetching
+ * into L2 (cp.async.bulk.prefetch.L2) the experts of `next` most likely to be hit at
+ * next's coming step: next's experts with hits > 0 at its most recent step, ranked by
+ * (hits desc, id asc) by next's own bookkeeping kernel, up to budget_bytes. Each CTA
+ * of the persistent FFN issues its share once it has no more work, so the prefetch fills
+ * the FFN tail, the combine and next's routing, when HBM would otherwise be idle.
+ *   next:            the context of the layer called after `ctx` (same device); NULL or
+ *                    budget_bytes == 0 disables. `next` must outlive `ctx` or be unset.
+ *   next_device_all: the packed experts `next` is called with ([E, 3HF], device).
+ * It is a cache hint only: outputs are bitwise unchanged. Nothing is prefetched before
+ * `next` has run one step. Returns TIDE_EINVAL on a null ctx, negative budget,
+ * different devices, or next != NULL with next_device_all == NULL.
+ * ------------------------------------------------------------------------ */
+TIDE_API tide_status tide_ctx_set_prefetch(tide_ctx* ctx, tide_ctx* next,
+                                           const void* next_device_all, int64_t budget_bytes);
+
+/* ------------------------------------------------------------------------
  * NEXT-2: refresh-interval model (Eq. 4-7), host-only.
  *   io(tau)   = c_io * (B*T/tau) * (1 - (1-d)^tau)                      (Eq. 5)
  *   miss(tau) = c_miss * T * B * f(tau), f(tau) = (1/tau) sum_{j<tau} (1-(1-d)^j)

@@ -31,6 +31,7 @@ constexpr int kTileM = 128;
 constexpr int kATile = kTileM * 128;           // 16 KB: 128 rows x 128 B (one K block)
 constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 128 B
 constexpr int kStageBytes = 2 * kATile + kBTile;
+constexpr int kPfPiece = 64 * 1024;  // bytes per L2 bulk prefetch
 constexpr int kMaxEntriesSmem = 1280;          // work entries built per CTA (E + N*k/128 + ...)
 constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem;
 
@@ -48,6 +49,12 @@ struct FfnParams {
   // off[e] = prefix of counts in id order, then the shared expert (rows N*k + n).
   const int* cnt;        // [E] per-expert token counts (build mode), or [2][E] with par
   const int* par;        // nullable: route's parity word, this step's counts = cnt[par^1]
+  // NEXT-3 prefetch of the next layer (pf_base == nullptr: off)
+  const uint8_t* pf_base;  // next layer's packed experts (device_all)
+  const int* pf_list;      // next layer's experts ranked by hits at its previous step
+  const int* pf_n;         // number of ranked (hit) experts
+  int pf_max;              // budget in experts
+  long long pf_xb;         // bytes per packed expert
   const int* slot_of;    // [E] pool slot (nullptr: slot = e)
   int* off_out;          // [E] row offsets written by CTA 0 (build mode; read by combine)
   const int4* entries;   // global mode: host-built list
@@ -311,6 +318,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       }
     }
     if (tr && lane == 0) { tr[2] = globaltimer_ns(); tr[4] = n_items; }
+    // NEXT-3 cross-layer prefetch: this CTA has no more work, so its share of the next
+    // layer's most-hit experts (ranked by that layer's book at its previous step) is pulled
+    // into L2 while the FFN drains and the combine / next routing leave HBM idle.
+    // Piece i of the ranked byte range goes to CTA i % grid, so the first CTAs to finish
+    // cover the highest-ranked experts first.  A cache hint only: values are unaffected.
+    if (p.pf_base) {
+      const int n = min(__ldcg(p.pf_n), p.pf_max);
+      const long long ppe = (p.pf_xb + kPfPiece - 1) / kPfPiece;
+      const long long pieces = (long long)n * ppe;
+      for (long long i = blockIdx.x + (long long)gridDim.x * lane; i < pieces;
+           i += (long long)gridDim.x * 32) {
+        const int j = (int)(i / ppe);
+        const long long q = (i - (long long)j * ppe) * kPfPiece;
+        const int e = __ldcg(p.pf_list + j);
+        const uint32_t bytes = (uint32_t)min((long long)kPfPiece, p.pf_xb - q);
+        prefetch_l2_bulk(p.pf_base + (size_t)e * p.pf_xb + q, bytes);
+      }
+    }
   } else if (warp == 1 && lane == 0) {
     // ===================== MMA issuer (one thread) =====================
     int stage = 0, islot = 0, acc = 0;

@@ -90,6 +90,8 @@ struct RouteParams {
 struct BookParams {
   const int* cnt;       // [E] hits, or [2][E] selected by par (see RouteParams)
   const int* par;       // nullable: cnt is double-buffered, this step's half = par^1
+  int* pf_list;         // nullable (NEXT-3): experts with hits > 0 ranked by (hits desc, id asc)
+  int* pf_n;            //   and their number; read by the previous layer's FFN next step
   const unsigned* mask; // [E * NW]
   unsigned* mask_rw;    // same, zeroed after use
   const int* topk_idx;  // [N,k]
@@ -361,6 +363,21 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
     s_pl[e] = p.placement_in[e] != 0;  // incumbents (overwritten below)
   }
   __syncthreads();
+  if (p.pf_list) {  // NEXT-3: rank this step's hit experts for the previous layer's prefetch
+    for (int e = tid; e < E; e += blockDim.x) {
+      const int he = s_hits[e];
+      if (he > 0) {
+        int r = 0;
+        for (int f = 0; f < E; ++f) {
+          const int hf = s_hits[f];
+          r += (hf > he) || (hf == he && f < e);
+        }
+        p.pf_list[r] = e;  // hit experts occupy ranks 0..U-1
+      }
+    }
+    const int u = __syncthreads_count(tid < E && s_hits[tid] > 0);  // E <= blockDim
+    if (tid == 0) *p.pf_n = u;
+  }
   if (p.refresh) {  // rank(e) = #{f : key[f] > key[e] or (== and [incumbent f] or f < e)}
     const int S = max(1, (int)blockDim.x / E);   // threads per expert
     const int seg = (E + S - 1) / S;

@@ -121,6 +121,13 @@ struct tide_ctx {
   int* pair_slot = nullptr;
   int* cnt = nullptr;        // [2][E] per-expert token counts (double-buffered, see cnt_par)
   int* cnt_par = nullptr;    // [2] device parity word + route completion counter
+  // NEXT-3 cross-layer prefetch
+  int* pf_list = nullptr;    // [E] this layer's hit experts ranked by hits (written by book)
+  int* pf_n = nullptr;       // [1] their number
+  bool pf_target = false;    // some other context prefetches for this one: book ranks
+  tide_ctx* pf_next = nullptr;         // the layer this context prefetches for
+  const void* pf_weights = nullptr;    // its packed experts (device_all)
+  int pf_max = 0;                      // budget in experts
   int* list = nullptr;       // [E * maxN] per-expert token lists
   unsigned* mask = nullptr;  // [E * NWmax] per-expert token bitmasks
   int* g_cnt = nullptr;      // [maxN + 2] route-kernel last-CTA counters
@@ -277,7 +284,7 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv, c->counter_acc, c->cnt_par};
+                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -352,6 +359,8 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->pair_slot, sizeof(int) * N * k);
   ALLOC(c->cnt, sizeof(int) * 2 * E);
   ALLOC(c->cnt_par, sizeof(int) * 2);
+  ALLOC(c->pf_list, sizeof(int) * E);
+  ALLOC(c->pf_n, sizeof(int));
   ALLOC(c->list, sizeof(int) * (size_t)E * N);
   ALLOC(c->mask, sizeof(unsigned) * E * c->NWmax);
   ALLOC(c->g_cnt, sizeof(int) * (N + 2));
@@ -519,7 +528,8 @@ static tide_status ensure_pool(tide_ctx* c) {
 static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
                               int N, cudaStream_t st, bool ep_local = false,
-                              unsigned long long* trace = nullptr, const int* par = nullptr) {
+                              unsigned long long* trace = nullptr, const int* par = nullptr,
+                              bool prefetch = false) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -529,6 +539,18 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.map_h = c->map_h;
   p.cnt = cnt;
   p.par = par;
+  p.pf_base = nullptr;
+  p.pf_list = nullptr;
+  p.pf_n = nullptr;
+  p.pf_max = 0;
+  p.pf_xb = 0;
+  if (prefetch && c->pf_next && c->pf_weights && c->pf_max > 0) {
+    p.pf_base = static_cast<const uint8_t*>(c->pf_weights);
+    p.pf_list = c->pf_next->pf_list;
+    p.pf_n = c->pf_next->pf_n;
+    p.pf_max = c->pf_max;
+    p.pf_xb = (long long)c->pf_next->expert_bytes;
+  }
   p.slot_of = slot_of;
   p.off_out = c->off;
   p.entries = entries;
@@ -611,6 +633,8 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   BookParams b;
   b.cnt = cnt;
   b.par = par;
+  b.pf_list = (c->pf_target && !E_override) ? c->pf_list : nullptr;
+  b.pf_n = c->pf_n;
   b.mask = c->mask;
   b.mask_rw = c->mask;
   b.topk_idx = c->topk;
@@ -908,7 +932,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   if (N > 0) {
     s = launch_ffn(c, c->cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
                    c->ffn_ctrl + 1, N, st, false,
-                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par);
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par,
+                   !pool_mode);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
@@ -999,7 +1024,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     return fail(TIDE_ECAPACITY, "capacity %d outside [1, %d] (per rank)", capacity, c->El);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CU_TRY(cudaSetDevice(c->device));
-  const int E = c->E, k = c->k, H = c->H, maxN = c->maxN, R = c->rows_all, El = c->El;
+  const int k = c->k, H = c->H, maxN = c->maxN, R = c->rows_all, El = c->El;
   const int refresh = (step % interval) == 0;
   tide_status s = ensure_weight_maps(c, local_experts, El, shared ? shared_w : nullptr);
   if (s != TIDE_OK) return s;
@@ -1132,6 +1157,26 @@ tide_status tide_trace_stats(const int32_t* counts, int32_t T, int32_t E, int32_
   CU_TRY(cudaGetLastError());
   tide_trace_step_kernel<<<T, 1024, 2 * E, st>>>(counts, T, E, B, unique, drift);
   CU_TRY(cudaGetLastError());
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_set_prefetch(tide_ctx* c, tide_ctx* next, const void* next_device_all,
+                                  int64_t budget_bytes) {
+  if (!c) return fail(TIDE_EINVAL, "null context");
+  if (budget_bytes < 0) return fail(TIDE_EINVAL, "budget_bytes %lld < 0", (long long)budget_bytes);
+  if (next && next->device != c->device)
+    return fail(TIDE_EINVAL, "next context is on device %d, this one on %d", next->device, c->device);
+  if (next && !next_device_all) return fail(TIDE_EINVAL, "next_device_all is null");
+  if (!next || budget_bytes == 0) {
+    c->pf_next = nullptr;
+    c->pf_weights = nullptr;
+    c->pf_max = 0;
+    return TIDE_OK;
+  }
+  c->pf_next = next;
+  c->pf_weights = next_device_all;
+  c->pf_max = (int)std::min<int64_t>(next->E, budget_bytes / (int64_t)next->expert_bytes);
+  next->pf_target = true;
   return TIDE_OK;
 }
 

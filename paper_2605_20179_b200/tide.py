@@ -125,6 +125,8 @@ def lib():
                                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p]
         L.tide_ctx_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.tide_ctx_set_prefetch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_int64]
         L.tide_ctx_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(PhaseTimes)]
         _lib = L
     return _lib
@@ -214,6 +216,14 @@ class Context:
         t = PhaseTimes()
         _check(lib().tide_ctx_get_timing(self.handle, ctypes.byref(t)))
         return t.as_dict()
+
+    def set_prefetch(self, next_ctx: "Context | None", next_device_all=None,
+                     budget_bytes: int = 0):
+        """tide_ctx_set_prefetch: prefetch `next_ctx`'s likely experts into L2 at the end of
+        this context's FFN (NEXT-3); None / 0 disables."""
+        _check(lib().tide_ctx_set_prefetch(
+            self.handle, next_ctx.handle if next_ctx is not None else None,
+            _ptr(next_device_all) if next_device_all is not None else None, int(budget_bytes)))
 
     def moe_step(self, block_hidden, router_w, *, device_all=None, host_master=None,
                  shared_w=None, placement, step: int, interval: int, capacity: int | None = None,

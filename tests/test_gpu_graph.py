@@ -93,3 +93,27 @@ def test_graph_replay_equals_eager(interval):
                 assert torch.equal(L["pl"], pl), (blk, t)
                 assert torch.equal(L["out"].view(torch.int16), o.view(torch.int16)), (blk, t)
             i += 1
+
+
+def test_cross_layer_prefetch_is_bitwise_neutral():
+    """NEXT-3 prefetch (tide_ctx_set_prefetch, ring over the stack) is a cache hint: every
+    output, hit count and placement equals the run without it, bit for bit."""
+    from paper_2605_20179_b200 import tide
+    T = SHAPE.steps
+    plain, pf = _stack(53), _stack(53)
+    n = len(pf)
+    for i, L in enumerate(pf):
+        nx = pf[(i + 1) % n]
+        L["ctx"].set_prefetch(nx["ctx"], nx["lay"].device_all, 1 << 30)
+    for t in range(T):
+        for A, B in zip(plain, pf):
+            _layer_step(A, t, 2)
+            _layer_step(B, t, 2)
+            torch.cuda.synchronize()
+            assert torch.equal(A["out"].view(torch.int16), B["out"].view(torch.int16)), t
+            assert torch.equal(A["hits"], B["hits"]) and torch.equal(A["pl"], B["pl"])
+    with pytest.raises(tide.TideError):
+        pf[0]["ctx"].set_prefetch(pf[1]["ctx"], pf[1]["lay"].device_all, -1)
+    with pytest.raises(tide.TideError):
+        pf[0]["ctx"].set_prefetch(pf[1]["ctx"], None, 1 << 20)
+    pf[0]["ctx"].set_prefetch(None)  # disable

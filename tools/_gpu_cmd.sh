@@ -1,4 +1,5 @@
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python tools/timeline.py mini 16 2>&1 | tail -14
-timeout 600 python bench.py --steps 192 --warmup 32 --no-cpu --no-e2e --graph > gpurun_out/bench_graph.json 2>gpurun_out/bench_graph.err; python -c "
-import json; d=json.load(open('gpurun_out/bench_graph.json')); print('graph', d['value'], d['ms_per_step'], d['roofline']['frac'], d['phases_us_per_layer_step'])"
+timeout 900 python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err; echo "bench rc=$?"; cat gpurun_out/bench_default.json | tail -c 2500
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err; echo "ref rc=$?"; tail -c 800 gpurun_out/bench_ref.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tide --csv --log-file gpurun_out/launches_r01_graph.csv python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?"
+python tools/launches.py gpurun_out/launches_r01_graph.csv
