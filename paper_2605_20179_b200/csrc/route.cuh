@@ -230,6 +230,53 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
     }
 }
 
+// Shared tail of both route kernels: arrive on the token group's counter; the group's last
+// CTA runs phase 2 (top-k a2, histogram + token lists a3) for its tokens; the last phase-2
+// CTA of the grid flips the count parity (all CTAs have read it by then).
+template <int EPL>
+__device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int par, int n0, int n1,
+                                           unsigned long long* tr, int& s_flag) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = p.E;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    if (tr) tr[1] = globaltimer_ns();
+    __threadfence();
+    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  if (tid == 0) {
+    p.g_cnt[blockIdx.y] = 0;
+    if (tr) tr[2] = globaltimer_ns();
+  }
+
+  // ================= phase 2: top-k of this token group (a2) + histogram (a3)
+  // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
+  // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
+  for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
+    float v[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+    }
+    route_token<EPL>(p, cnt, n, v);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (tr) tr[3] = globaltimer_ns();
+    __threadfence();
+    if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
+      *p.g_done = 0;
+      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
+      __threadfence();
+    }
+  }
+}
+
 // grid (ceil(E/8), ceil(N/tpc)), 256 threads.  EPL = logits per lane in the top-k
 // (power of two >= E/32).
 template <typename T, int EPL>
@@ -301,43 +348,94 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
       }
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    if (tr) tr[1] = globaltimer_ns();
-    __threadfence();
-    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_flag) return;
-  __threadfence();
-  if (tid == 0) {
-    p.g_cnt[blockIdx.y] = 0;
-    if (tr) tr[2] = globaltimer_ns();
-  }
+  route_tail<EPL>(p, cnt, par, n0, n1, tr, s_flag);
+}
 
-  // ================= phase 2: top-k of this token group (a2) + histogram (a3)
-  // Lane l holds logits e = l + 32 i (i < EPL), sorts them by (value desc, id asc) in
-  // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
-  for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
-    float v[EPL];
+// bf16 variant, phase 1 on the tensor cores: CTA = 16 experts x 8 tokens, the 8 warps
+// split H; each warp issues m16n8k16 MMAs with C = 0 and adds every 16-product partial into
+// fp64 registers, then the 8 warp partials are summed in warp order in fp64 and rounded
+// to fp32 once (R-17: the only fp32 roundings are inside each 16-term MMA sum).
+// k is permuted identically in A and B: lane (g, c) loads 16 contiguous bytes at
+// k = kb + 8c of expert rows g, g+8 and token g; its bf16 pairs 0,1 feed k-slots
+// {2c, 2c+8} of the first MMA, pairs 2,3 those of the second, so the two MMAs cover
+// exactly k in [kb, kb+32).  grid (E/16, ceil(N/8)), 256 threads; needs E % 16 == 0,
+// H % 256 == 0.
+template <int EPL>
+__global__ void __launch_bounds__(kRouteThreads) tide_route_tc_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_flag;
+  __shared__ double s_red[kRouteThreads / 32][32][4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = p.E, N = p.N, H = p.H;
+  const int n0 = blockIdx.y * 8, n1 = min(N, n0 + 8), e0 = blockIdx.x * 16;
+  pdl_wait();
+  pdl_trigger();
+  unsigned long long* tr =
+      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
+  const int par = __ldcg(p.par);
+  int* cnt = p.cnt2 + par * E;
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
+    for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
+  }
+  // ================= phase 1: router logits (a1)
+  {
+    constexpr int G = 8;  // 32-wide k blocks in flight per warp
+    const int g = lane >> 2, c = lane & 3;
+    const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.wr);
+    const uint4* wa = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g) * H);
+    const uint4* wb = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g + 8) * H);
+    const uint4* xt = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) +
+                                                     (size_t)min(n0 + g, N - 1) * H);
+    const int kw = H / (kRouteThreads / 32), kbeg = warp * kw;  // this warp's k range
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kb = kbeg; kb < kbeg + kw; kb += 32 * G) {
+      uint4 A0[G], A1[G], B[G];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
-      const int e = lane + 32 * i;
-      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+      for (int i = 0; i < G; ++i) {
+        const int k = kb + 32 * i;
+        if (k < kbeg + kw) {
+          const int q = (k >> 3) + c;  // uint4 index of k + 8c
+          A0[i] = __ldg(wa + q);
+          A1[i] = __ldg(wb + q);
+          B[i] = __ldg(xt + q);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (kb + 32 * i < kbeg + kw) {
+          float d[4];
+          mma_bf16_m16n8k16(d, A0[i].x, A1[i].x, A0[i].y, A1[i].y, B[i].x, B[i].y);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r] += (double)d[r];
+          mma_bf16_m16n8k16(d, A0[i].z, A1[i].z, A0[i].w, A1[i].w, B[i].z, B[i].w);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r] += (double)d[r];
+        }
+      }
     }
-    route_token<EPL>(p, cnt, n, v);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (tr) tr[3] = globaltimer_ns();
-    __threadfence();
-    if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
-      *p.g_done = 0;
-      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
-      __threadfence();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s_red[warp][lane][r] = acc[r];
+    // x_in copy (the FFN's gather source) by the first expert tile of each token group
+    if (blockIdx.x == 0) {
+      const int per_row = H / 8;  // uint4 per row
+      for (int i = tid; i < (n1 - n0) * per_row; i += blockDim.x) {
+        const int n = n0 + i / per_row, q = i % per_row;
+        reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.x_in) + (size_t)n * H)[q] =
+            __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) + (size_t)n * H) + q);
+      }
+    }
+    __syncthreads();
+    if (tid < 128) {  // output (expert row r, token col q): lane (r&7)*4 + q/2, reg 2(r>>3) + (q&1)
+      const int r = tid >> 3, q = tid & 7;
+      const int ln = (r & 7) * 4 + (q >> 1), rg = (r >> 3) * 2 + (q & 1);
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < kRouteThreads / 32; ++w) v += s_red[w][ln][rg];
+      if (n0 + q < N) p.logits[(size_t)(n0 + q) * E + e0 + r] = (float)v;
     }
   }
+  route_tail<EPL>(p, cnt, par, n0, n1, tr, s_flag);
 }
 
 // One CTA (1024 threads): a4 placement and a5 bookkeeping from the hit counts.

@@ -689,6 +689,24 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.n_zero = 1 + c->max_entries;
   rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
                                        : nullptr;
+  // bf16 routers run phase 1 on the tensor cores (16 experts x 8 tokens per CTA);
+  // TIDE_ROUTER_CC=1 forces the CUDA-core kernel (A/B measurement)
+  if (c->bf16 && E % 16 == 0 && H % 256 == 0 && !getenv("TIDE_ROUTER_CC")) {
+    rp.tpc = 8;
+    const dim3 grid(E / 16, std::max(1, (N + 7) / 8));
+    cudaError_t le;
+    switch (route_epl(E)) {
+      case 1: le = launch_pdl(tide_route_tc_kernel<1>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      case 2: le = launch_pdl(tide_route_tc_kernel<2>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      case 4: le = launch_pdl(tide_route_tc_kernel<4>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      case 8: le = launch_pdl(tide_route_tc_kernel<8>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      case 16: le = launch_pdl(tide_route_tc_kernel<16>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      default: le = launch_pdl(tide_route_tc_kernel<32>, grid, dim3(kRouteThreads), 0, st, rp); break;
+    }
+    CU_TRY(le);
+    c->launches++;
+    return TIDE_OK;
+  }
   {
     const dim3 grid((E + kRouterWarps - 1) / kRouterWarps, std::max(1, (N + rp.tpc - 1) / rp.tpc));
     cudaError_t le;

@@ -37,7 +37,8 @@ tpc = int(os.environ.get("TIDE_ROUTE_TPC", 4 if N <= 64 else 8))
 ny = max(1, (N + tpc - 1) // tpc)
 rows = []
 for li, r in enumerate(res):
-    rt = r.debug["route_trace"].cpu().numpy().reshape(-1, 4).astype(np.int64)[: ((E + 7) // 8) * ny]
+    rt = r.debug["route_trace"].cpu().numpy().reshape(-1, 4).astype(np.int64)
+    rt = rt[rt[:, 0] > 0]
     ft = r.debug["ffn_trace"].cpu().numpy().reshape(-1, 8).astype(np.int64)
     ft = ft[ft[:, 0] > 0]
     last = rt[rt[:, 2] > 0]
