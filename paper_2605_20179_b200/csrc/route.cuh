@@ -360,8 +360,11 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
 // {2c, 2c+8} of the first MMA, pairs 2,3 those of the second, so the two MMAs cover
 // exactly k in [kb, kb+32).  grid (E/16, ceil(N/8)), 256 threads; needs E % 16 == 0,
 // H % 256 == 0.
-template <int EPL>
-__global__ void __launch_bounds__(kRouteThreads) tide_route_tc_kernel(const __grid_constant__ RouteParams p) {
+// G = 32-wide k blocks in flight per warp per round (8: one load round at H=2048);
+// MINB = resident CTAs per SM the register budget is sized for.  (G=4 with 4 CTAs/SM was
+// measured for the 512-CTA sweep grid: one wave, but no faster end to end.)
+template <int EPL, int G, int MINB>
+__global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(const __grid_constant__ RouteParams p) {
   __shared__ int s_flag;
   __shared__ double s_red[kRouteThreads / 32][32][4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -380,7 +383,6 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_tc_kernel(const __gr
   }
   // ================= phase 1: router logits (a1)
   {
-    constexpr int G = 8;  // 32-wide k blocks in flight per warp
     const int g = lane >> 2, c = lane & 3;
     const __nv_bfloat16* wr = static_cast<const __nv_bfloat16*>(p.wr);
     const uint4* wa = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g) * H);

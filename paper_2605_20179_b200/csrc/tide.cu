@@ -695,14 +695,17 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
     rp.tpc = 8;
     const dim3 grid(E / 16, std::max(1, (N + 7) / 8));
     cudaError_t le;
+#define TC_LAUNCH(EP) \
+  le = launch_pdl(tide_route_tc_kernel<EP, 8, 1>, grid, dim3(kRouteThreads), 0, st, rp)
     switch (route_epl(E)) {
-      case 1: le = launch_pdl(tide_route_tc_kernel<1>, grid, dim3(kRouteThreads), 0, st, rp); break;
-      case 2: le = launch_pdl(tide_route_tc_kernel<2>, grid, dim3(kRouteThreads), 0, st, rp); break;
-      case 4: le = launch_pdl(tide_route_tc_kernel<4>, grid, dim3(kRouteThreads), 0, st, rp); break;
-      case 8: le = launch_pdl(tide_route_tc_kernel<8>, grid, dim3(kRouteThreads), 0, st, rp); break;
-      case 16: le = launch_pdl(tide_route_tc_kernel<16>, grid, dim3(kRouteThreads), 0, st, rp); break;
-      default: le = launch_pdl(tide_route_tc_kernel<32>, grid, dim3(kRouteThreads), 0, st, rp); break;
+      case 1: TC_LAUNCH(1); break;
+      case 2: TC_LAUNCH(2); break;
+      case 4: TC_LAUNCH(4); break;
+      case 8: TC_LAUNCH(8); break;
+      case 16: TC_LAUNCH(16); break;
+      default: TC_LAUNCH(32); break;
     }
+#undef TC_LAUNCH
     CU_TRY(le);
     c->launches++;
     return TIDE_OK;
