@@ -1,7 +1,6 @@
-timeout 300 python tools/router_err.py
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python tools/timeline.py sweep 16 2>&1 | tail -4
-for cfg in sweep mini; do
-  timeout 600 python bench.py --config $cfg --steps 96 --warmup 32 --no-cpu --no-e2e > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print('$cfg', d['value'], d['ms_per_step'], d['roofline']['frac'], d['phases_us_per_layer_step']['router_ms'])"
+for cap in 64 128; do
+timeout 1200 python bench.py --config flash1 --layers 16 --capacity $cap --interval 4 --steps 32 --warmup 4 --cpu-seconds 8 > gpurun_out/bench_flash_c$cap.json 2>gpurun_out/bench_flash_c$cap.err; echo "cap $cap rc=$?"
+python -c "
+import json; d=json.load(open('gpurun_out/bench_flash_c$cap.json')); print('flash C=$cap', d['value'], d['ms_per_step'], d['io'], d['step_split'], d['e2e']['value'] if d['e2e'] else None)"
+tail -2 gpurun_out/bench_flash_c$cap.err
 done
