@@ -225,6 +225,46 @@ TIDE_API tide_status tide_moe_step_ep(tide_ctx* ctx, const void* block_hidden, i
                                       int32_t* hit_counts, uint8_t* placement_out,
                                       tide_step_stats* stats, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Peer-memory expert parallelism (NEXT-3 "fused NVLink dispatch/combine", SURVEY 8(f);
+ * the exchange of SURVEY 8(e) without NCCL on the data path).  Same step, same
+ * arguments, same results (bitwise equal to the NCCL path for a fixed world): the
+ * dispatch is a kernel that stores each token row, its top-k ids and gates straight
+ * into every rank's symmetric region (P2P stores over NVLink / NVSwitch), and the
+ * per-source partial sums are stored by the partial kernel straight into the source
+ * rank's receive buffer; each CTA then arrives on a counter in the destination
+ * (release, system scope) that the consuming kernel waits on (acquire).
+ *
+ * Setup, on every rank, per layer context:
+ *   tide_ctx_create_ep_p2p(desc, device, rank, world, &ctx)    (world <= 8)
+ *   tide_ctx_ep_export(ctx, handle, &base)   -> this rank's IPC handle
+ *                                               (tide_ep_handle_bytes() bytes) and base
+ *   exchange the handles (e.g. torch.distributed all_gather), then
+ *   tide_ctx_ep_connect(ctx, handles, bases)  handles: world * handle_bytes in rank
+ *                                               order; bases: nullable array of
+ *                                               world pointers; a non-null entry is
+ *                                               used as that peer's region directly
+ *                                               (same process: single-GPU emulation)
+ *   barrier across ranks before the first tide_moe_step_ep.
+ * Ownership: the context owns its symmetric region and the peer mappings it opened
+ * (closed by tide_ctx_destroy; destroy on every rank only after all ranks finished
+ * their last step).  A waiting kernel gives up after 20 s, records the failure in the
+ * context's error word (tide_ctx_ep_error) and returns without hanging the GPU; the
+ * step's outputs are then undefined.  Not capturable across ranks' differing call
+ * counts: every rank must call tide_moe_step_ep once per layer-step, in the same order.
+ * ------------------------------------------------------------------------ */
+TIDE_API tide_status tide_ctx_create_ep_p2p(const tide_layer_desc* desc, int32_t device,
+                                            int32_t rank, int32_t world, tide_ctx** out);
+TIDE_API size_t tide_ep_handle_bytes(void);
+/* handle (nullable): out, tide_ep_handle_bytes() bytes; base (nullable): out, device ptr. */
+TIDE_API tide_status tide_ctx_ep_export(tide_ctx* ctx, void* handle, void** base);
+/* TIDE_EINVAL if not a peer-memory context, already connected, or a peer has neither a
+ * handle nor a base; TIDE_ECUDA if cudaIpcOpenMemHandle fails. */
+TIDE_API tide_status tide_ctx_ep_connect(tide_ctx* ctx, const void* handles,
+                                         const void* const* bases);
+/* *err = 1 if a peer-memory wait timed out since the context was created (synchronous). */
+TIDE_API tide_status tide_ctx_ep_error(tide_ctx* ctx, int32_t* err);
+
 /* Per-phase device timing (CUDA events recorded on the step's stream at phase
  * boundaries).  Enabling resets the accumulators; tide_ctx_get_timing waits
  * for the recorded events, adds their elapsed times and clears them.

@@ -106,4 +106,230 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
   }
 }
 
+
+// ---------------------------------------------------------------- peer-memory EP
+// tide_ctx_create_ep_p2p: the same EP step with the two exchanges done by the kernels
+// themselves over peer memory (NVLink / NVSwitch P2P stores into the other ranks'
+// symmetric regions, one counter arrival per CTA) instead of NCCL collectives:
+//   tide_ep_push_kernel     dispatch: each (token row, destination) CTA stores the row of
+//                           x_in, its top-k ids and gates into the destination's x_all /
+//                           topk_all / gates_all at [rank*maxN + n], then arrives on the
+//                           destination's dispatch counter
+//   tide_ep_lists_kernel    (p2p) waits until all P*maxN rows have arrived
+//   tide_ep_partial_kernel  (p2p) stores each source row's partial straight into the
+//                           source rank's recv[rank][n] (and the local experts' counts into
+//                           its hits_all), then arrives on its combine counter
+//   tide_ep_final_kernel    (p2p) waits for all P*maxN*ceil(H/512) partial CTAs, then the
+//                           same rank-order sum as the NCCL path (bitwise identical)
+// Counters are double-buffered by the step parity word the route kernel flips; the lists
+// kernel of a step zeroes the other parity's counters (their last readers finished a step
+// ago; their next writers need this step's partials first).  A waiting CTA gives up after
+// kEpWaitNs, records the failure in the context's error word and returns (no GPU hang).
+constexpr int kEpMaxWorld = 8;
+constexpr unsigned long long kEpWaitNs = 20000000000ull;  // 20 s
+
+struct EpPeers {
+  char* base[kEpMaxWorld];  // symmetric region of every rank (own included), rank order
+};
+
+struct EpSymLayout {  // byte offsets inside a rank's symmetric region
+  size_t x_all, topk_all, gates_all, recv, hits_all, ctr, total;
+  // ctr: [0..1] dispatch arrivals by parity, [2..3] combine arrivals by parity, [4] error
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Thread 0 spins until *ctr >= target (acquire, system scope); the CTA then proceeds.
+// Returns false (for every thread) on timeout, after recording it in *err.
+__device__ __forceinline__ bool ep_wait_all(const unsigned* ctr, unsigned target, unsigned* err) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    if (ld_acquire_sys_u32(ctr) < target) {
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys_u32(ctr) < target) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > kEpWaitNs) {
+          atomicExch(err, 1u);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Every thread's stores of this CTA become visible to the destination GPU before the arrival.
+__device__ __forceinline__ void ep_arrive(unsigned* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    red_release_sys_add_u32(ctr, 1u);
+  }
+}
+
+struct EpPushParams {
+  EpPeers peers;
+  EpSymLayout lay;
+  const uint4* x_in;   // [maxN, row_bytes] this rank's hidden states (route kernel's copy)
+  const int* topk;     // [maxN, k] (rows >= N hold -1)
+  const float* gates;  // [maxN, k]
+  const int* par;      // step parity word (flipped by the route kernel)
+  int rank, maxN, N, k, row_u4;
+};
+
+// grid (maxN, P), 128 threads: CTA (n, dst) sends row n to rank dst.
+__global__ void __launch_bounds__(128) tide_ep_push_kernel(const EpPushParams p) {
+  pdl_wait();
+  const int n = blockIdx.x, dst = blockIdx.y;
+  char* b = p.peers.base[dst];
+  const size_t row = (size_t)p.rank * p.maxN + n;
+  if (n < p.N) {
+    uint4* dx = reinterpret_cast<uint4*>(b + p.lay.x_all) + row * p.row_u4;
+    const uint4* sx = p.x_in + (size_t)n * p.row_u4;
+    for (int i = threadIdx.x; i < p.row_u4; i += blockDim.x) dx[i] = __ldcg(sx + i);
+  }
+  if (threadIdx.x < p.k) {
+    reinterpret_cast<int*>(b + p.lay.topk_all)[row * p.k + threadIdx.x] =
+        __ldcg(p.topk + (size_t)n * p.k + threadIdx.x);
+    reinterpret_cast<float*>(b + p.lay.gates_all)[row * p.k + threadIdx.x] =
+        __ldcg(p.gates + (size_t)n * p.k + threadIdx.x);
+  }
+  const int par = __ldcg(p.par);
+  ep_arrive(reinterpret_cast<unsigned*>(b + p.lay.ctr) + par);
+}
+
+// p2p variant of tide_ep_lists_kernel: wait for the P*maxN dispatched rows first.
+__global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
+    char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int k, int e0,
+    int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
+    int* __restrict__ pslot_all) {
+  unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
+  const int par = __ldcg(par_word);
+  if (!ep_wait_all(ctr + par, target, ctr + 4)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // other parity: free for the next step
+    ctr[par ^ 1] = 0u;
+    ctr[2 + (par ^ 1)] = 0u;
+  }
+  const int* topk_all = reinterpret_cast<const int*>(sym + lay.topk_all);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= rows * k) return;
+  const int e = __ldcg(topk_all + q);
+  if (e >= e0 && e < e0 + El) {
+    const int s = atomicAdd(&cnt_l[e - e0], 1);
+    list_l[(size_t)(e - e0) * list_stride + s] = q / k;
+    pslot_all[q] = s;
+  } else {
+    pslot_all[q] = -1;
+  }
+}
+
+// p2p variant of tide_ep_partial_kernel: grid (P*maxN, ceil(H/512)); row's partial goes to
+// the source rank (row / maxN) at recv[rank][row % maxN]; the first row CTA of each source
+// also delivers this rank's local-expert counts into the source's hits_all[e0 .. e0+El).
+__global__ void __launch_bounds__(128) tide_ep_partial_p2p_kernel(
+    EpPeers peers, EpSymLayout lay, const float* __restrict__ y,
+    const int* __restrict__ topk_all, const float* __restrict__ gates_all,
+    const int* __restrict__ pslot_all, const int* __restrict__ off_l,
+    const int* __restrict__ cnt_l, const int* par_word, int rank, int maxN, int k, int H,
+    int e0, int El) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x, lane = threadIdx.x & 31;
+  const int src = row / maxN, n = row - src * maxN;
+  char* b = peers.base[src];
+  const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  int r_j = -1;
+  float g_j = 0.f;
+  if (lane < k) {
+    const int q = row * k + lane;
+    const int e = __ldcg(topk_all + q);
+    if (e >= e0 && e < e0 + El) {
+      r_j = __ldcg(off_l + (e - e0)) + __ldcg(pslot_all + q);
+      g_j = __ldcg(gates_all + q);
+    }
+  }
+  const bool valid = c < H;
+  const int cc = valid ? c : 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < k; ++j) {
+    const int r = __shfl_sync(0xffffffffu, r_j, j);
+    const float g = __shfl_sync(0xffffffffu, g_j, j);
+    if (r < 0) continue;
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)r * H + cc));
+    acc.x = fmaf(g, v.x, acc.x);
+    acc.y = fmaf(g, v.y, acc.y);
+    acc.z = fmaf(g, v.z, acc.z);
+    acc.w = fmaf(g, v.w, acc.w);
+  }
+  if (valid)
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(b + lay.recv) +
+                               ((size_t)rank * maxN + n) * H + c) = acc;
+  if (n == 0 && blockIdx.y == 0) {
+    int* hits = reinterpret_cast<int*>(b + lay.hits_all) + e0;
+    for (int i = threadIdx.x; i < El; i += blockDim.x) hits[i] = __ldcg(cnt_l + i);
+  }
+  const int par = __ldcg(par_word);
+  ep_arrive(reinterpret_cast<unsigned*>(b + lay.ctr) + 2 + par);
+}
+
+// p2p variant of tide_ep_final_kernel: grid (max(N,1), ceil(H/512)).  CTA (0,0) also
+// copies the global hits.
+template <typename T>
+__global__ void __launch_bounds__(128) tide_ep_final_p2p_kernel(
+    char* sym, EpSymLayout lay, const int* par_word, unsigned target, const float* __restrict__ y,
+    T* __restrict__ out, int32_t* __restrict__ hit_counts, int E, int N, int P, int maxN, int H,
+    int shared_row0) {
+  pdl_wait();
+  pdl_trigger();
+  unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
+  const int par = __ldcg(par_word);
+  const int n = blockIdx.x;
+  if (n >= N && !(n == 0 && blockIdx.y == 0)) return;
+  if (!ep_wait_all(ctr + 2 + par, target, ctr + 4)) return;
+  if (n == 0 && blockIdx.y == 0) {
+    const int* hits = reinterpret_cast<const int*>(sym + lay.hits_all);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) hit_counts[i] = __ldcg(hits + i);
+  }
+  if (n >= N) return;
+  const float* recv = reinterpret_cast<const float*>(sym + lay.recv);
+  const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  if (c >= H) return;
+  float4 acc = __ldcg(reinterpret_cast<const float4*>(recv + (size_t)n * H + c));
+  for (int p = 1; p < P; ++p) {  // rank order (same arithmetic as tide_ep_final_kernel)
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(recv + ((size_t)p * maxN + n) * H + c));
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  if (shared_row0 >= 0) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(shared_row0 + n) * H + c));
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  T* o = out + (size_t)n * H + c;
+  if constexpr (sizeof(T) == 2) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(o) = pk;
+  } else {
+    *reinterpret_cast<float4*>(o) = acc;
+  }
+}
+
 }  // namespace tide

@@ -184,6 +184,12 @@ struct tide_ctx {
   float* partial = nullptr;     // [P*maxN, H] per-source partial sums (send buffer)
   float* recv = nullptr;        // [P*maxN, H] partials for this rank's tokens
   CUtensorMap map_x_all;
+  // peer-memory EP (tide_ctx_create_ep_p2p): x_all/topk_all/gates_all/recv live in `sym`
+  bool p2p = false, connected = false;
+  char* sym = nullptr;
+  EpSymLayout lay{};
+  EpPeers peers{};
+  std::vector<void*> ipc_opened;  // peers' regions opened with cudaIpcOpenMemHandle
 
   // per-phase timing (tide_ctx_set_timing)
   bool timing = false;
@@ -279,6 +285,14 @@ void tide_ctx_destroy(tide_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->side) cudaStreamSynchronize(c->side);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->p2p) {  // these live inside the symmetric region
+    c->x_all = nullptr;
+    c->topk_all = nullptr;
+    c->gates_all = nullptr;
+    c->recv = nullptr;
+    cudaFree(c->sym);
+  }
   void* dev[] = {c->logits, c->topk,     c->gates,   c->pair_slot, c->cnt,    c->list,
                  c->mask,   c->g_cnt,    c->off,     c->pos,       c->order,  c->offsets,
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
@@ -424,7 +438,7 @@ tide_status tide_nccl_unique_id(void* out) {
 
 static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
                                       const void* nccl_id, tide_ctx* parent, int32_t rank,
-                                      int32_t world, tide_ctx** out) {
+                                      int32_t world, tide_ctx** out, bool p2p = false) {
   if (!out) return fail(TIDE_EINVAL, "null argument");
   *out = nullptr;
   tide_status s = validate_desc(d);
@@ -447,23 +461,51 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
   c->El = El;
   c->e0 = rank * El;
   const int N = c->maxN, k = c->k, R = c->rows_all;
-  ALLOC(c->x_all, c->eb * (size_t)R * c->H);
-  ALLOC(c->topk_all, sizeof(int) * (size_t)R * k);
-  ALLOC(c->gates_all, sizeof(float) * (size_t)R * k);
+  if (p2p) {  // one allocation holds everything the peers write (one IPC handle)
+    if (world > kEpMaxWorld) {
+      tide_ctx_destroy(c);
+      return fail(TIDE_EUNSUPPORTED, "peer-memory EP supports world <= %d", kEpMaxWorld);
+    }
+    auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    EpSymLayout& L = c->lay;
+    L.x_all = 0;
+    L.topk_all = up(L.x_all + c->eb * (size_t)R * c->H);
+    L.gates_all = up(L.topk_all + sizeof(int) * (size_t)R * k);
+    L.recv = up(L.gates_all + sizeof(float) * (size_t)R * k);
+    L.hits_all = up(L.recv + sizeof(float) * (size_t)R * c->H);
+    L.ctr = up(L.hits_all + sizeof(int) * (size_t)c->E);
+    L.total = up(L.ctr + sizeof(unsigned) * 8);
+    c->p2p = true;
+    ALLOC(c->sym, L.total);
+    c->x_all = c->sym + L.x_all;
+    c->topk_all = reinterpret_cast<int*>(c->sym + L.topk_all);
+    c->gates_all = reinterpret_cast<float*>(c->sym + L.gates_all);
+    c->recv = reinterpret_cast<float*>(c->sym + L.recv);
+    c->peers.base[rank] = c->sym;
+    c->connected = world == 1;
+  } else {
+    ALLOC(c->x_all, c->eb * (size_t)R * c->H);
+    ALLOC(c->topk_all, sizeof(int) * (size_t)R * k);
+    ALLOC(c->gates_all, sizeof(float) * (size_t)R * k);
+  }
   ALLOC(c->pslot_all, sizeof(int) * (size_t)R * k);
   ALLOC(c->cnt_l, sizeof(int) * El);
   ALLOC(c->list_l, sizeof(int) * (size_t)El * R);
   ALLOC(c->off_l, sizeof(int) * El);
   ALLOC(c->hits_l, sizeof(int) * El);
-  ALLOC(c->partial, sizeof(float) * (size_t)R * c->H);
-  ALLOC(c->recv, sizeof(float) * (size_t)R * c->H);
+  if (!p2p) {
+    ALLOC(c->partial, sizeof(float) * (size_t)R * c->H);
+    ALLOC(c->recv, sizeof(float) * (size_t)R * c->H);
+  }
   (void)N;
   if (make_map(&c->map_x_all, c->x_all, c->bf16, c->H, R, 1) != TIDE_OK) {
     std::string m = g_err;
     tide_ctx_destroy(c);
     return fail(TIDE_ECUDA, "%s", m.c_str());
   }
-  if (parent) {
+  if (p2p) {
+    cudaDeviceSynchronize();  // the zeroed region is visible before any peer connects
+  } else if (parent) {
     c->comm = parent->comm;
   } else {
     ncclUniqueId id;
@@ -484,6 +526,58 @@ tide_status tide_ctx_create_ep(const tide_layer_desc* d, int32_t device, const v
                                int32_t rank, int32_t world, tide_ctx** out) {
   if (!nccl_id) return fail(TIDE_EINVAL, "nccl_unique_id is null");
   return ctx_create_ep_impl(d, device, nccl_id, nullptr, rank, world, out);
+}
+
+tide_status tide_ctx_create_ep_p2p(const tide_layer_desc* d, int32_t device, int32_t rank,
+                                   int32_t world, tide_ctx** out) {
+  return ctx_create_ep_impl(d, device, nullptr, nullptr, rank, world, out, true);
+}
+
+size_t tide_ep_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+tide_status tide_ctx_ep_export(tide_ctx* c, void* handle, void** base) {
+  if (!c || !c->p2p) return fail(TIDE_EINVAL, "not a peer-memory EP context");
+  if (!handle && !base) return fail(TIDE_EINVAL, "handle and base are both null");
+  CU_TRY(cudaSetDevice(c->device));
+  if (handle) {
+    cudaIpcMemHandle_t h;
+    CU_TRY(cudaIpcGetMemHandle(&h, c->sym));
+    memcpy(handle, &h, sizeof(h));
+  }
+  if (base) *base = c->sym;
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_ep_connect(tide_ctx* c, const void* handles, const void* const* bases) {
+  if (!c || !c->p2p) return fail(TIDE_EINVAL, "not a peer-memory EP context");
+  if (c->connected && c->world > 1) return fail(TIDE_EINVAL, "context already connected");
+  if (!handles && !bases) return fail(TIDE_EINVAL, "handles and bases are both null");
+  CU_TRY(cudaSetDevice(c->device));
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    if (bases && bases[p]) {
+      c->peers.base[p] = static_cast<char*>(const_cast<void*>(bases[p]));
+      continue;
+    }
+    if (!handles) return fail(TIDE_EINVAL, "no handle or base for rank %d", p);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + (size_t)p * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    CU_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(ptr);
+    c->peers.base[p] = static_cast<char*>(ptr);
+  }
+  c->connected = true;
+  return TIDE_OK;
+}
+
+tide_status tide_ctx_ep_error(tide_ctx* c, int32_t* err) {
+  if (!c || !c->p2p || !err) return fail(TIDE_EINVAL, "not a peer-memory EP context / null err");
+  unsigned v = 0;
+  CU_TRY(cudaSetDevice(c->device));
+  CU_TRY(cudaMemcpy(&v, c->sym + c->lay.ctr + 4 * sizeof(unsigned), sizeof(v), cudaMemcpyDeviceToHost));
+  *err = (int32_t)v;
+  return TIDE_OK;
 }
 
 tide_status tide_ctx_create_ep_like(const tide_layer_desc* d, tide_ctx* parent, tide_ctx** out) {
@@ -1034,6 +1128,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
                              int32_t capacity, void* out, int32_t* hit_counts,
                              uint8_t* placement_out, tide_step_stats* stats, void* stream) {
   if (!c || !c->ep) return fail(TIDE_EINVAL, "not an expert-parallel context");
+  if (c->p2p && !c->connected)
+    return fail(TIDE_EINVAL, "peer-memory EP context not connected (tide_ctx_ep_connect)");
   if (N < 0 || N > c->maxN) return fail(TIDE_EINVAL, "num_tokens %d outside [0, %d]", N, c->maxN);
   const bool shared = (c->d.flags & TIDE_SHARED_EXPERT) != 0;
   if (!local_experts || !wr || !placement || !placement_out || !hit_counts || (N > 0 && (!x || !out)))
@@ -1061,17 +1157,40 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
   if (N < maxN) CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
   // dispatch: every rank's tokens and routing to every rank (fixed counts, no host sync)
-  const ncclDataType_t xt = c->bf16 ? ncclBfloat16 : ncclFloat32;
-  NC_TRY(ncclGroupStart());
-  NC_TRY(ncclAllGather(c->x_in, c->x_all, (size_t)maxN * H, xt, c->comm, st));
-  NC_TRY(ncclAllGather(c->topk, c->topk_all, (size_t)maxN * k, ncclInt32, c->comm, st));
-  NC_TRY(ncclAllGather(c->gates, c->gates_all, (size_t)maxN * k, ncclFloat32, c->comm, st));
-  NC_TRY(ncclGroupEnd());
+  const int nY = (H + 511) / 512;
+  if (c->p2p) {  // kernels store into the peers' symmetric regions (ep.cuh)
+    EpPushParams pp;
+    pp.peers = c->peers;
+    pp.lay = c->lay;
+    pp.x_in = static_cast<const uint4*>(c->x_in);
+    pp.topk = c->topk;
+    pp.gates = c->gates;
+    pp.par = c->cnt_par;
+    pp.rank = c->rank;
+    pp.maxN = maxN;
+    pp.N = N;
+    pp.k = k;
+    pp.row_u4 = (int)(c->eb * H / 16);
+    CU_TRY(launch_pdl(tide_ep_push_kernel, dim3(maxN, c->world), dim3(128), 0, st, pp));
+    c->launches++;
+  } else {
+    const ncclDataType_t xt = c->bf16 ? ncclBfloat16 : ncclFloat32;
+    NC_TRY(ncclGroupStart());
+    NC_TRY(ncclAllGather(c->x_in, c->x_all, (size_t)maxN * H, xt, c->comm, st));
+    NC_TRY(ncclAllGather(c->topk, c->topk_all, (size_t)maxN * k, ncclInt32, c->comm, st));
+    NC_TRY(ncclAllGather(c->gates, c->gates_all, (size_t)maxN * k, ncclFloat32, c->comm, st));
+    NC_TRY(ncclGroupEnd());
+  }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[2], st));
   // local experts' token lists over all rows; their counts are the global hits (R-18)
   CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
-  tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El, c->cnt_l,
-                                                          c->list_l, R, c->pslot_all);
+  if (c->p2p)
+    tide_ep_lists_p2p_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(
+        c->sym, c->lay, c->cnt_par, (unsigned)(c->world * maxN), R, k, c->e0, El, c->cnt_l,
+        c->list_l, R, c->pslot_all);
+  else
+    tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El,
+                                                            c->cnt_l, c->list_l, R, c->pslot_all);
   CU_TRY(cudaGetLastError());
   c->launches++;
   s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El,
@@ -1082,27 +1201,49 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
-  // a10: per-source partial sums, all-to-all, rank-order sum
-  CU_TRY(launch_pdl(tide_ep_partial_kernel, dim3(R, (H + 511) / 512), dim3(128), 0, st,
-                    (const float*)c->y_perm, (const int*)c->topk_all, (const float*)c->gates_all,
-                    (const int*)c->pslot_all, (const int*)c->off_l, c->partial, k, H, c->e0, El));
-  c->launches++;
-  NC_TRY(ncclAlltoAll(c->partial, c->recv, (size_t)maxN * H, ncclFloat32, c->comm, st));
-  if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
-  if (N > 0) {
-    const dim3 grid(N, (H + 511) / 512);
-    const int srow = shared ? R * k : -1;
-    if (c->bf16)
-      CU_TRY(launch_pdl(tide_ep_final_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
-                        (const float*)c->recv, (const float*)c->y_perm,
-                        static_cast<__nv_bfloat16*>(out), c->world, maxN, H, srow));
-    else
-      CU_TRY(launch_pdl(tide_ep_final_kernel<float>, grid, dim3(128), 0, st, (const float*)c->recv,
-                        (const float*)c->y_perm, static_cast<float*>(out), c->world, maxN, H,
-                        srow));
+  // a10: per-source partial sums, exchange, rank-order sum
+  const int srow = shared ? R * k : -1;
+  if (c->p2p) {
+    CU_TRY(launch_pdl(tide_ep_partial_p2p_kernel, dim3(R, nY), dim3(128), 0, st, c->peers, c->lay,
+                      (const float*)c->y_perm, (const int*)c->topk_all,
+                      (const float*)c->gates_all, (const int*)c->pslot_all,
+                      (const int*)c->off_l, (const int*)c->cnt_l, (const int*)c->cnt_par,
+                      c->rank, maxN, k, H, c->e0, El));
     c->launches++;
+    if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
+    const dim3 grid(std::max(N, 1), nY);
+    const unsigned tgt = (unsigned)(c->world * maxN * nY);
+    if (c->bf16)
+      CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<__nv_bfloat16>, grid, dim3(128), 0, st, c->sym,
+                        c->lay, (const int*)c->cnt_par, tgt, (const float*)c->y_perm,
+                        static_cast<__nv_bfloat16*>(out), hit_counts, c->E, N, c->world, maxN, H,
+                        srow));
+    else
+      CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<float>, grid, dim3(128), 0, st, c->sym, c->lay,
+                        (const int*)c->cnt_par, tgt, (const float*)c->y_perm,
+                        static_cast<float*>(out), hit_counts, c->E, N, c->world, maxN, H, srow));
+    c->launches++;
+  } else {
+    CU_TRY(launch_pdl(tide_ep_partial_kernel, dim3(R, nY), dim3(128), 0, st,
+                      (const float*)c->y_perm, (const int*)c->topk_all, (const float*)c->gates_all,
+                      (const int*)c->pslot_all, (const int*)c->off_l, c->partial, k, H, c->e0, El));
+    c->launches++;
+    NC_TRY(ncclAlltoAll(c->partial, c->recv, (size_t)maxN * H, ncclFloat32, c->comm, st));
+    if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
+    if (N > 0) {
+      const dim3 grid(N, nY);
+      if (c->bf16)
+        CU_TRY(launch_pdl(tide_ep_final_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
+                          (const float*)c->recv, (const float*)c->y_perm,
+                          static_cast<__nv_bfloat16*>(out), c->world, maxN, H, srow));
+      else
+        CU_TRY(launch_pdl(tide_ep_final_kernel<float>, grid, dim3(128), 0, st, (const float*)c->recv,
+                          (const float*)c->y_perm, static_cast<float*>(out), c->world, maxN, H,
+                          srow));
+      c->launches++;
+    }
+    NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
   }
-  NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
   if (c->timing) {
     CU_TRY(cudaEventRecord(rec.ev[6], st));
     rec.launches = c->launches - launches0;
