@@ -64,6 +64,9 @@ def parse():
                          "-1 = default (32 MB when all experts are in HBM), 0 = off")
     ap.add_argument("--ep", action="store_true",
                     help="expert parallelism over the ranks (tide_moe_step_ep) instead of replicas")
+    ap.add_argument("--p2p", action="store_true",
+                    help="with --ep: dispatch/combine by the kernels over peer memory "
+                         "(tide_ctx_create_ep_p2p) instead of NCCL collectives")
     return ap.parse_args()
 
 
@@ -213,7 +216,17 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         w = {"device_all": packed} if not pool_mode else {"host_master": packed.cpu().pin_memory()}
         if pool_mode:
             del packed
-        if ep:
+        if ep and args.p2p:
+            ctx = tide.EPPeerContext(desc, rank, world, local_rank)
+            hs = [None] * world
+            mine = ctx.export()
+            if world > 1:
+                torch.distributed.all_gather_object(hs, mine[0])
+                ctx.connect(handles=hs)
+                torch.distributed.barrier()
+            else:
+                ctx.connect(bases=[mine[1]])
+        elif ep:
             ctx = tide.EPContext(desc, uid[0] if l == 0 else None, rank, world, local_rank,
                                  like=None if l == 0 else layers[0]["ctx"])
         else:
@@ -258,7 +271,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     for i in range(args.warmup):
         bench_step(i)
     torch.cuda.synchronize()
-    if not args.eager and not pool_mode and not ep:  # NEXT-3: one graph per block step t, every layer-step of the stack in it
+    if not args.eager and not pool_mode and (not ep or args.p2p):  # NEXT-3: one graph per block step t, every layer-step of the stack in it
         gl = []
         for t in range(T):
             gr = torch.cuda.CUDAGraph()
@@ -454,7 +467,8 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                       "tokens_per_layer_step": N, "num_experts": E, "top_k": k, "hidden": H,
                       "ffn": F, "capacity": cap, "interval": args.interval,
                       "parallelism": (f"expert parallel x{world} (E/P = {El} experts per rank, "
-                                      "NCCL all-gather dispatch + all-to-all combine)") if ep
+                                      + ("peer-memory dispatch/combine kernels)" if args.p2p else
+                                         "NCCL all-gather dispatch + all-to-all combine)")) if ep
                       else f"replicas x{world} (each rank its own blocks)",
                       "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
                             "through the stack between reuses",

@@ -257,13 +257,15 @@ def ep_step(L: Layer, P: int, x: np.ndarray, k: int, placement_in: np.ndarray, s
     wg = _ptr_array([L.wg[e] for e in range(E)], keep)
     wu = _ptr_array([L.wu[e] for e in range(E)], keep)
     wd = _ptr_array([L.wd[e] for e in range(E)], keep)
+    sh = [np.ascontiguousarray(a) for a in L.shared] if L.shared is not None else [None] * 3
     wr = np.ascontiguousarray(L.wr)
     pin = np.ascontiguousarray(placement_in, np.uint8)
     topk_idx = np.empty((N, k), np.int32)
     h = np.empty(E, np.int32)
     pout = np.empty(E, np.uint8)
     out = np.empty((N, H))
-    rc = lib().orc_ep_step(ctypes.byref(st), P, N, _p(x), _p(wr), wg, wu, wd, _p(pin), step,
+    rc = lib().orc_ep_step(ctypes.byref(st), P, N, _p(x), _p(wr), wg, wu, wd, _p(sh[0]),
+                           _p(sh[1]), _p(sh[2]), _p(pin), step,
                            interval, capacity_per_rank, _p(topk_idx), _p(h), _p(pout), _p(out))
     assert rc == 0
     return topk_idx, h, pout, out

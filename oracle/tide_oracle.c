@@ -279,6 +279,7 @@ int orc_io_step(int E, int lazy, const int32_t* hits, const uint8_t* placement_i
 /* ---------------- O11: expert-parallel emulation (R-18) ------------------ */
 int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
                 const void* const* wg, const void* const* wu, const void* const* wd,
+                const void* swg, const void* swu, const void* swd,
                 const uint8_t* placement_in, int step, int interval, int capacity_per_rank,
                 int32_t* topk_idx, int32_t* hits, uint8_t* placement_out, double* out) {
   const int E = L->num_experts, k = L->top_k, H = L->hidden;
@@ -311,6 +312,13 @@ int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
       }
     }
     for (size_t i = 0; i < (size_t)N * H; ++i) out[i] += part[i];
+  }
+  if (L->shared_expert) { /* R-16: the token's own rank adds its shared expert, weight 1 */
+    for (int n = 0; n < N; ++n) {
+      for (int h = 0; h < H; ++h) xn[h] = rd(x, L->act_dtype, (size_t)n * H + h);
+      orc_swiglu(H, L->ffn, xn, swg, swu, swd, L->weight_dtype, y);
+      for (int h = 0; h < H; ++h) out[(size_t)n * H + h] += y[h];
+    }
   }
   free(logits);
   free(gates);

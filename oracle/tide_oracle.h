@@ -101,9 +101,11 @@ int orc_io_step(int E, int lazy, const int32_t* hits, const uint8_t* placement_i
 /* O11 (P:460-462 future work; DESIGN R-18): expert-parallel emulation over
  * P ranks in one process.  Rank r owns experts [r*E/P, (r+1)*E/P); hits are
  * global; rank r's placement = top-C_r of its own experts by global hits;
- * out = sum over ranks (in rank order) of that rank's partial combine.    */
+ * out = sum over ranks (in rank order) of that rank's partial combine, plus the
+ * shared expert (R-16, weight 1) when L->shared_expert (swg/swu/swd, else unused). */
 int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
                 const void* const* wg, const void* const* wu, const void* const* wd,
+                const void* swg, const void* swu, const void* swd,
                 const uint8_t* placement_in, int step, int interval, int capacity_per_rank,
                 int32_t* topk_idx, int32_t* hits, uint8_t* placement_out, double* out);
 

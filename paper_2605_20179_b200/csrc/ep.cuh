@@ -185,7 +185,8 @@ struct EpPushParams {
   const int* topk;     // [maxN, k] (rows >= N hold -1)
   const float* gates;  // [maxN, k]
   const int* par;      // step parity word (flipped by the route kernel)
-  int rank, maxN, N, k, row_u4;
+  int* cnt_l;          // [El] zeroed here for tide_ep_lists_p2p_kernel (no memset node)
+  int rank, maxN, N, k, row_u4, El;
 };
 
 // grid (maxN, P), 128 threads: CTA (n, dst) sends row n to rank dst.
@@ -199,12 +200,15 @@ __global__ void __launch_bounds__(128) tide_ep_push_kernel(const EpPushParams p)
     const uint4* sx = p.x_in + (size_t)n * p.row_u4;
     for (int i = threadIdx.x; i < p.row_u4; i += blockDim.x) dx[i] = __ldcg(sx + i);
   }
-  if (threadIdx.x < p.k) {
+  if (threadIdx.x < p.k) {  // rows >= N carry no token: expert id -1
+    const bool tok = n < p.N;
     reinterpret_cast<int*>(b + p.lay.topk_all)[row * p.k + threadIdx.x] =
-        __ldcg(p.topk + (size_t)n * p.k + threadIdx.x);
+        tok ? __ldcg(p.topk + (size_t)n * p.k + threadIdx.x) : -1;
     reinterpret_cast<float*>(b + p.lay.gates_all)[row * p.k + threadIdx.x] =
-        __ldcg(p.gates + (size_t)n * p.k + threadIdx.x);
+        tok ? __ldcg(p.gates + (size_t)n * p.k + threadIdx.x) : 0.f;
   }
+  if (n == 0 && dst == 0)
+    for (int i = threadIdx.x; i < p.El; i += blockDim.x) p.cnt_l[i] = 0;
   const int par = __ldcg(p.par);
   ep_arrive(reinterpret_cast<unsigned*>(b + p.lay.ctr) + par);
 }
@@ -214,6 +218,7 @@ __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
     char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int k, int e0,
     int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
     int* __restrict__ pslot_all) {
+  pdl_wait();  // this rank's push (and its cnt_l zeroing) is complete
   unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
   const int par = __ldcg(par_word);
   if (!ep_wait_all(ctr + par, target, ctr + 4)) return;

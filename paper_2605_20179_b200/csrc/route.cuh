@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
     const uint4* wa = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g) * H);
     const uint4* wb = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g + 8) * H);
     const uint4* xt = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) +
-                                                     (size_t)min(n0 + g, N - 1) * H);
+                                                     (size_t)max(0, min(n0 + g, N - 1)) * H);
     const int kw = H / (kRouteThreads / 32), kbeg = warp * kw;  // this warp's k range
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int kb = kbeg; kb < kbeg + kw; kb += 32 * G) {

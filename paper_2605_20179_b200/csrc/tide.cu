@@ -234,6 +234,52 @@ static int route_epl(int E) {
   return epl;
 }
 
+// Load every kernel a peer-memory EP step launches now.  With lazy module loading the
+// first launch of a kernel can synchronise the device; a rank whose kernels spin on a peer
+// must never block on that between its own launches (CUDA_MODULE_LOADING=LAZY hazard for
+// producer/consumer kernels).
+template <typename F>
+static void touch(F* f) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, f);
+}
+static void preload_ep_p2p_kernels(const tide_ctx* c) {
+  const int epl = route_epl(c->E);
+  if (c->bf16 && c->E % 16 == 0 && c->H % 256 == 0) {
+    switch (epl) {
+      case 1: touch(tide_route_tc_kernel<1, 8, 1>); break;
+      case 2: touch(tide_route_tc_kernel<2, 8, 1>); break;
+      case 4: touch(tide_route_tc_kernel<4, 8, 1>); break;
+      case 8: touch(tide_route_tc_kernel<8, 8, 1>); break;
+      case 16: touch(tide_route_tc_kernel<16, 8, 1>); break;
+      default: touch(tide_route_tc_kernel<32, 8, 1>); break;
+    }
+  }
+#define TOUCH_ROUTE(TT)                                     \
+  switch (epl) {                                            \
+    case 1: touch(tide_route_kernel<TT, 1>); break;         \
+    case 2: touch(tide_route_kernel<TT, 2>); break;         \
+    case 4: touch(tide_route_kernel<TT, 4>); break;         \
+    case 8: touch(tide_route_kernel<TT, 8>); break;         \
+    case 16: touch(tide_route_kernel<TT, 16>); break;       \
+    default: touch(tide_route_kernel<TT, 32>); break;       \
+  }
+  if (c->bf16) {
+    TOUCH_ROUTE(__nv_bfloat16)
+    touch(tide_ffn_kernel<__nv_bfloat16>);
+    touch(tide_ep_final_p2p_kernel<__nv_bfloat16>);
+  } else {
+    TOUCH_ROUTE(float)
+    touch(tide_ffn_kernel<float>);
+    touch(tide_ep_final_p2p_kernel<float>);
+  }
+#undef TOUCH_ROUTE
+  touch(tide_book_kernel);
+  touch(tide_ep_push_kernel);
+  touch(tide_ep_lists_p2p_kernel);
+  touch(tide_ep_partial_p2p_kernel);
+}
+
 extern "C" {
 
 int32_t tide_abi_version(void) { return TIDE_ABI_VERSION; }
@@ -504,6 +550,7 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     return fail(TIDE_ECUDA, "%s", m.c_str());
   }
   if (p2p) {
+    preload_ep_p2p_kernels(c);
     cudaDeviceSynchronize();  // the zeroed region is visible before any peer connects
   } else if (parent) {
     c->comm = parent->comm;
@@ -758,7 +805,7 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
                                 tide_step_debug* dbg, cudaStream_t st) {
   const int E = c->E, k = c->k, H = c->H;
   RouteParams rp;
-  rp.x = x;
+  rp.x = N > 0 ? x : c->x_in;  // no tokens: a valid (unread) row for the clamped loads
   rp.wr = wr;
   rp.x_in = c->x_in;
   rp.logits = c->logits;
@@ -1155,7 +1202,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   s = launch_route(c, x, N, wr, nullptr, st);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[1], st));
-  if (N < maxN) CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
+  if (N < maxN && !c->p2p)
+    CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
   // dispatch: every rank's tokens and routing to every rank (fixed counts, no host sync)
   const int nY = (H + 511) / 512;
   if (c->p2p) {  // kernels store into the peers' symmetric regions (ep.cuh)
@@ -1171,6 +1219,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     pp.N = N;
     pp.k = k;
     pp.row_u4 = (int)(c->eb * H / 16);
+    pp.cnt_l = c->cnt_l;
+    pp.El = El;
     CU_TRY(launch_pdl(tide_ep_push_kernel, dim3(maxN, c->world), dim3(128), 0, st, pp));
     c->launches++;
   } else {
@@ -1183,19 +1233,25 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[2], st));
   // local experts' token lists over all rows; their counts are the global hits (R-18)
-  CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
-  if (c->p2p)
-    tide_ep_lists_p2p_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(
-        c->sym, c->lay, c->cnt_par, (unsigned)(c->world * maxN), R, k, c->e0, El, c->cnt_l,
-        c->list_l, R, c->pslot_all);
-  else
+  if (c->p2p) {  // cnt_l was zeroed by the push kernel
+    CU_TRY(launch_pdl(tide_ep_lists_p2p_kernel, dim3((R * k + 255) / 256), dim3(256), 0, st,
+                      c->sym, c->lay, (const int*)c->cnt_par, (unsigned)(c->world * maxN), R, k,
+                      c->e0, El, c->cnt_l, c->list_l, R, c->pslot_all));
+  } else {
+    CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
     tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El,
                                                             c->cnt_l, c->list_l, R, c->pslot_all);
-  CU_TRY(cudaGetLastError());
+    CU_TRY(cudaGetLastError());
+  }
   c->launches++;
-  s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, st, El,
-                  step);
+  // a4: placement of the local experts runs beside the FFN on the side stream (the FFN
+  // computes every hit local expert; placement' only drives I/O), joined before the end
+  CU_TRY(cudaEventRecord(c->ev_route, st));
+  CU_TRY(cudaStreamWaitEvent(c->side, c->ev_route, 0));
+  s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, c->side,
+                  El, step);
   if (s != TIDE_OK) return s;
+  CU_TRY(cudaEventRecord(c->ev_book, c->side));
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[3], st));
   // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
   s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true);
@@ -1244,6 +1300,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     }
     NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
   }
+  CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // placement_out / info valid with the stream
   if (c->timing) {
     CU_TRY(cudaEventRecord(rec.ev[6], st));
     rec.launches = c->launches - launches0;

@@ -29,7 +29,9 @@ EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert
             "tide_expert_bytes", "tide_pack_expert", "tide_ctx_create", "tide_ctx_destroy",
             "tide_moe_step", "tide_ctx_set_timing", "tide_ctx_get_timing", "tide_nccl_unique_id",
             "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep",
-            "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats")
+            "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats",
+            "tide_ctx_create_ep_p2p", "tide_ep_handle_bytes", "tide_ctx_ep_export",
+            "tide_ctx_ep_connect", "tide_ctx_ep_error")
 
 
 class TideError(RuntimeError):
@@ -128,6 +130,15 @@ def lib():
         L.tide_ctx_set_prefetch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_int64]
         L.tide_ctx_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(PhaseTimes)]
+        L.tide_ctx_create_ep_p2p.argtypes = [ctypes.POINTER(LayerDesc), ctypes.c_int32,
+                                             ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.POINTER(ctypes.c_void_p)]
+        L.tide_ep_handle_bytes.restype = ctypes.c_size_t
+        L.tide_ep_handle_bytes.argtypes = []
+        L.tide_ctx_ep_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.POINTER(ctypes.c_void_p)]
+        L.tide_ctx_ep_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.tide_ctx_ep_error.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
         _lib = L
     return _lib
 
@@ -332,6 +343,49 @@ class EPContext(Context):
             _ptr(placement_out), ctypes.byref(st) if st is not None else None,
             _stream_ptr(stream)))
         return StepOutputs(out, hit_counts, placement_out, st.as_dict() if st else None, None)
+
+
+class EPPeerContext(EPContext):
+    """tide_ctx_create_ep_p2p: expert-parallel context whose dispatch and combine are done by
+    the kernels over peer memory (no NCCL on the data path).  Connect it before stepping:
+    `export()` on every rank, exchange, `connect(handles, bases)` on every rank, barrier."""
+
+    def __init__(self, desc: LayerDesc, rank: int, world: int, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().tide_ctx_create_ep_p2p(ctypes.byref(desc), device, rank, world,
+                                            ctypes.byref(h)))
+        self.handle = h
+        self.desc = desc
+        self.rank, self.world = rank, world
+        self.local_experts = desc.num_experts // world
+        self.capacity = self.local_experts
+        self.device = device
+
+    def export(self) -> tuple[bytes, int]:
+        """(IPC handle bytes, device base pointer) of this rank's symmetric region."""
+        n = lib().tide_ep_handle_bytes()
+        buf = ctypes.create_string_buffer(n)
+        base = ctypes.c_void_p()
+        _check(lib().tide_ctx_ep_export(self.handle, buf, ctypes.byref(base)))
+        return buf.raw, int(base.value or 0)
+
+    def connect(self, handles: list[bytes] | None = None, bases: list[int | None] | None = None):
+        """handles: every rank's export()[0] in rank order (other processes); bases: every
+        rank's export()[1] where the region is directly addressable (same process)."""
+        n = lib().tide_ep_handle_bytes()
+        hb = None
+        if handles is not None:
+            hb = ctypes.create_string_buffer(b"".join(bytes(x).ljust(n, b"\0")[:n] for x in handles),
+                                             n * self.world)
+        bb = None
+        if bases is not None:
+            bb = (ctypes.c_void_p * self.world)(*[b or None for b in bases])
+        _check(lib().tide_ctx_ep_connect(self.handle, hb, bb))
+
+    def error(self) -> int:
+        v = ctypes.c_int32()
+        _check(lib().tide_ctx_ep_error(self.handle, ctypes.byref(v)))
+        return v.value
 
 
 def interval_cost(T: int, B: int, d: float, c_io: float, c_miss: float, tau: int):

@@ -117,13 +117,21 @@ def test_ep_protocol_world2_matches_single_device_oracle():
         assert err <= 1e-12 * max(scale, 1.0), (rank, err)
 
 
-def test_oracle_ep_emulation_world2_matches_single_device():
-    """O11 with P=2 on the same shapes (one process)."""
-    lt = g.layer_np(SHAPE, 5)
-    L = oracle.Layer(lt.wr, lt.wg, lt.wu, lt.wd)
-    x = g.block_hidden_np(SHAPE, 100, steps=1)[0]
-    E, k = SHAPE.num_experts, SHAPE.top_k
+@pytest.mark.parametrize("shared", [False, True])
+@pytest.mark.parametrize("P_", [2, 4])
+def test_oracle_ep_emulation_matches_single_device(shared, P_):
+    """O11 with P ranks on the same shapes (one process): EP moves bytes, not math, so it
+    equals the single-device oracle step, shared expert (R-16) included."""
+    sh = g.Shape("ep", 8, 3, 64, 64, 1, 6, steps=2, dtype="bf16", shared_expert=shared)
+    lt = g.layer_np(sh, 5)
+    L = oracle.Layer(lt.wr, lt.wg, lt.wu, lt.wd, lt.shared)
+    x = g.block_hidden_np(sh, 100, steps=1)[0]
+    E, k = sh.num_experts, sh.top_k
     single = oracle.moe_step(L, x, k, np.zeros(E, np.uint8), 0, 1, E)
-    t, h, pout, out = oracle.ep_step(L, P, x, k, np.zeros(E, np.uint8), 0, 1, E // P)
+    t, h, pout, out = oracle.ep_step(L, P_, x, k, np.zeros(E, np.uint8), 0, 1, E // P_)
     assert (h == single.hits).all() and pout.all()
     assert np.allclose(out, single.out, rtol=1e-13, atol=1e-14)
+    if shared:  # the shared term is really there: dropping it changes the output
+        L0 = oracle.Layer(lt.wr, lt.wg, lt.wu, lt.wd)
+        assert not np.allclose(oracle.ep_step(L0, P_, x, k, np.zeros(E, np.uint8), 0, 1,
+                                              E // P_)[3], out)
