@@ -330,7 +330,9 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     skp_ms = [m for m, r in per if not r]
     step_split = {"ms_refresh_step": round(sum(ref_ms) / max(1, len(ref_ms)), 4),
                   "ms_skipped_step": round(sum(skp_ms) / max(1, len(skp_ms)), 4),
-                  "refresh_steps": len(ref_ms), "skipped_steps": len(skp_ms)}
+                  "refresh_steps": len(ref_ms), "skipped_steps": len(skp_ms),
+                  "p50_ms_step": round(float(np.percentile([m for m, _ in per], 50)), 4),
+                  "p90_ms_step": round(float(np.percentile([m for m, _ in per], 90)), 4)}
     layer_steps = args.steps * Lyr
     value = N * layer_steps * world / (ms / 1e3)
 

@@ -12,6 +12,7 @@
 // Hits of the local experts are global (all ranks' tokens); ncclAllGather assembles [E].
 #pragma once
 #include "ptx.cuh"
+#include "route.cuh"
 
 namespace tide {
 
@@ -110,12 +111,12 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
 // ---------------------------------------------------------------- peer-memory EP
 // tide_ctx_create_ep_p2p: the same EP step with the two exchanges done by the kernels
 // themselves over peer memory (NVLink / NVSwitch P2P stores into the other ranks'
-// symmetric regions, one counter arrival per CTA) instead of NCCL collectives:
-//   tide_ep_push_kernel     dispatch: each (token row, destination) CTA stores the row of
-//                           x_in, its top-k ids and gates into the destination's x_all /
-//                           topk_all / gates_all at [rank*maxN + n], then arrives on the
-//                           destination's dispatch counter
-//   tide_ep_lists_kernel    (p2p) waits until all P*maxN rows have arrived
+// symmetric regions, counter arrivals with release semantics) instead of NCCL collectives:
+//   route kernel (route.cuh) dispatch fused into the router: X rows, top-k ids, gates and
+//                           the token count go straight into every rank's x_all /
+//                           topk_all / gates_all / ntok at [rank*maxN + n]; one arrival per
+//                           source rank on each destination's dispatch counter
+//   tide_ep_lists_kernel    (p2p) waits until all P sources have arrived
 //   tide_ep_partial_kernel  (p2p) stores each source row's partial straight into the
 //                           source rank's recv[rank][n] (and the local experts' counts into
 //                           its hits_all), then arrives on its combine counter
@@ -132,8 +133,11 @@ struct EpPeers {
   char* base[kEpMaxWorld];  // symmetric region of every rank (own included), rank order
 };
 
+static_assert(kEpMaxWorld == kRouteEpMax, "route.cuh and ep.cuh disagree on the max world");
+
 struct EpSymLayout {  // byte offsets inside a rank's symmetric region
-  size_t x_all, topk_all, gates_all, recv, hits_all, ctr, total;
+  size_t x_all, topk_all, gates_all, recv, hits_all, ntok, ctr, total;
+  // ntok: [P] tokens each source rank dispatched this step (rows >= ntok[src] are stale)
   // ctr: [0..1] dispatch arrivals by parity, [2..3] combine arrivals by parity, [4] error
 };
 
@@ -178,47 +182,13 @@ __device__ __forceinline__ void ep_arrive(unsigned* ctr) {
   }
 }
 
-struct EpPushParams {
-  EpPeers peers;
-  EpSymLayout lay;
-  const uint4* x_in;   // [maxN, row_bytes] this rank's hidden states (route kernel's copy)
-  const int* topk;     // [maxN, k] (rows >= N hold -1)
-  const float* gates;  // [maxN, k]
-  const int* par;      // step parity word (flipped by the route kernel)
-  int* cnt_l;          // [El] zeroed here for tide_ep_lists_p2p_kernel (no memset node)
-  int rank, maxN, N, k, row_u4, El;
-};
-
-// grid (maxN, P), 128 threads: CTA (n, dst) sends row n to rank dst.
-__global__ void __launch_bounds__(128) tide_ep_push_kernel(const EpPushParams p) {
-  pdl_wait();
-  const int n = blockIdx.x, dst = blockIdx.y;
-  char* b = p.peers.base[dst];
-  const size_t row = (size_t)p.rank * p.maxN + n;
-  if (n < p.N) {
-    uint4* dx = reinterpret_cast<uint4*>(b + p.lay.x_all) + row * p.row_u4;
-    const uint4* sx = p.x_in + (size_t)n * p.row_u4;
-    for (int i = threadIdx.x; i < p.row_u4; i += blockDim.x) dx[i] = __ldcg(sx + i);
-  }
-  if (threadIdx.x < p.k) {  // rows >= N carry no token: expert id -1
-    const bool tok = n < p.N;
-    reinterpret_cast<int*>(b + p.lay.topk_all)[row * p.k + threadIdx.x] =
-        tok ? __ldcg(p.topk + (size_t)n * p.k + threadIdx.x) : -1;
-    reinterpret_cast<float*>(b + p.lay.gates_all)[row * p.k + threadIdx.x] =
-        tok ? __ldcg(p.gates + (size_t)n * p.k + threadIdx.x) : 0.f;
-  }
-  if (n == 0 && dst == 0)
-    for (int i = threadIdx.x; i < p.El; i += blockDim.x) p.cnt_l[i] = 0;
-  const int par = __ldcg(p.par);
-  ep_arrive(reinterpret_cast<unsigned*>(b + p.lay.ctr) + par);
-}
-
-// p2p variant of tide_ep_lists_kernel: wait for the P*maxN dispatched rows first.
+// p2p variant of tide_ep_lists_kernel: wait for the P sources' dispatch first; rows past a
+// source's token count hold stale routing and are skipped (pslot -1).
 __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
-    char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int k, int e0,
-    int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
+    char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int maxN, int k,
+    int e0, int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
     int* __restrict__ pslot_all) {
-  pdl_wait();  // this rank's push (and its cnt_l zeroing) is complete
+  pdl_wait();  // this rank's route kernel (and its cnt_l zeroing) is complete
   unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
   const int par = __ldcg(par_word);
   if (!ep_wait_all(ctr + par, target, ctr + 4)) return;
@@ -229,7 +199,9 @@ __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
   const int* topk_all = reinterpret_cast<const int*>(sym + lay.topk_all);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= rows * k) return;
-  const int e = __ldcg(topk_all + q);
+  const int row = q / k, src = row / maxN;
+  const bool live = row - src * maxN < __ldcg(reinterpret_cast<const int*>(sym + lay.ntok) + src);
+  const int e = live ? __ldcg(topk_all + q) : -1;
   if (e >= e0 && e < e0 + El) {
     const int s = atomicAdd(&cnt_l[e - e0], 1);
     list_l[(size_t)(e - e0) * list_stride + s] = q / k;
@@ -256,11 +228,11 @@ __global__ void __launch_bounds__(128) tide_ep_partial_p2p_kernel(
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
   int r_j = -1;
   float g_j = 0.f;
-  if (lane < k) {
+  if (lane < k) {  // pslot >= 0 iff the pair is live and routed to a local expert
     const int q = row * k + lane;
-    const int e = __ldcg(topk_all + q);
-    if (e >= e0 && e < e0 + El) {
-      r_j = __ldcg(off_l + (e - e0)) + __ldcg(pslot_all + q);
+    const int sl = __ldcg(pslot_all + q);
+    if (sl >= 0) {
+      r_j = __ldcg(off_l + (__ldcg(topk_all + q) - e0)) + sl;
       g_j = __ldcg(gates_all + q);
     }
   }

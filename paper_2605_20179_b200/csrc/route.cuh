@@ -65,6 +65,8 @@ struct RouteInfo {
   // followed by: hits[E] (int32), placement_out[E] (u8)
 };
 
+constexpr int kRouteEpMax = 8;  // == kEpMaxWorld (ep.cuh)
+
 struct RouteParams {
   const void* x;        // [N,H] caller's block hidden states
   const void* wr;       // [E,H] router
@@ -85,6 +87,16 @@ struct RouteParams {
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
   int n_zero;
   unsigned long long* trace;  // debug: 4 timestamps per CTA (nullable)
+  // Peer-memory EP dispatch fused into the router (tide_ctx_create_ep_p2p; ep_P == 0: off).
+  // Every CTA stores its slice of its token rows of X into every rank's x_all; each token
+  // group's phase-2 CTA stores the group's top-k ids and gates; the grid's last CTA stores
+  // this rank's token count and arrives (release, system scope) on every rank's dispatch
+  // counter for the new parity.  Row of token n of this rank in x_all: ep_rank*maxN + n.
+  int ep_P, ep_rank;
+  char* ep_base[kRouteEpMax];  // symmetric region of every rank
+  size_t ep_off_x, ep_off_topk, ep_off_gates, ep_off_ntok, ep_off_ctr;
+  int* zero_j;                 // EP: local-expert counts zeroed by CTA (0,0)
+  int n_zero_j;
 };
 
 struct BookParams {
@@ -242,6 +254,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   __syncthreads();
   if (tid == 0) {
     if (tr) tr[1] = globaltimer_ns();
+    if (p.ep_P) __threadfence_system();  // this CTA's x stores to the peers (route_ep_push_x)
     __threadfence();
     s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
   }
@@ -266,14 +279,51 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     route_token<EPL>(p, cnt, n, v);
   }
   __syncthreads();
+  if (p.ep_P) {  // dispatch this group's routing to every rank
+    const int k = p.k, rows = n1 - n0, tot = p.ep_P * rows * k;
+    for (int i = tid; i < tot; i += blockDim.x) {
+      const int j = i % k, n = n0 + (i / k) % rows, dst = i / (k * rows);
+      const size_t q = ((size_t)p.ep_rank * p.maxN + n) * k + j;
+      reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_topk)[q] = __ldcg(p.topk_idx + (size_t)n * k + j);
+      reinterpret_cast<float*>(p.ep_base[dst] + p.ep_off_gates)[q] = __ldcg(p.gates + (size_t)n * k + j);
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
+    if (p.ep_P) __threadfence_system();
     __threadfence();
     if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
       __threadfence();
+      if (p.ep_P) {  // every group's stores precede this point (g_done chain): arrive
+        for (int dst = 0; dst < p.ep_P; ++dst)
+          reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
+        __threadfence_system();
+        for (int dst = 0; dst < p.ep_P; ++dst)
+          asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(
+                           reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + (par ^ 1)),
+                       "r"(1u) : "memory");
+      }
     }
+  }
+}
+
+// Peer-memory EP dispatch of X: CTA (bx, by) stores uint4 columns [bx*per, (bx+1)*per) of
+// its token rows [n0, n1) into every rank's x_all (the grid's CTAs share each row).
+template <typename T>
+__device__ __forceinline__ void route_ep_push_x(const RouteParams& p, int n0, int n1) {
+  if (!p.ep_P) return;
+  const int u4 = p.H * (int)sizeof(T) / 16;
+  const int per = (u4 + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int q0 = blockIdx.x * per, w = min(u4, q0 + per) - q0, rows = n1 - n0;
+  if (w <= 0 || rows <= 0) return;
+  const int tot = p.ep_P * rows * w;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int q = q0 + i % w, n = n0 + (i / w) % rows, dst = i / (w * rows);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) + (size_t)n * p.H) + q);
+    reinterpret_cast<uint4*>(p.ep_base[dst] + p.ep_off_x)[((size_t)p.ep_rank * p.maxN + n) * u4 + q] = v;
   }
 }
 
@@ -295,6 +345,7 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
+    for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
   }
 
   // ================= phase 1: router logits (a1)
@@ -348,6 +399,7 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
       }
     }
   }
+  route_ep_push_x<T>(p, n0, n1);
   route_tail<EPL>(p, cnt, par, n0, n1, tr, s_flag);
 }
 
@@ -380,6 +432,7 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
+    for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
   }
   // ================= phase 1: router logits (a1)
   {
@@ -437,6 +490,7 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
       if (n0 + q < N) p.logits[(size_t)(n0 + q) * E + e0 + r] = (float)v;
     }
   }
+  route_ep_push_x<__nv_bfloat16>(p, n0, n1);
   route_tail<EPL>(p, cnt, par, n0, n1, tr, s_flag);
 }
 

@@ -275,7 +275,6 @@ static void preload_ep_p2p_kernels(const tide_ctx* c) {
   }
 #undef TOUCH_ROUTE
   touch(tide_book_kernel);
-  touch(tide_ep_push_kernel);
   touch(tide_ep_lists_p2p_kernel);
   touch(tide_ep_partial_p2p_kernel);
 }
@@ -492,6 +491,8 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
   if (world < 1 || rank < 0 || rank >= world) return fail(TIDE_EINVAL, "rank %d / world %d", rank, world);
   if (d->num_experts % world)
     return fail(TIDE_EUNSUPPORTED, "num_experts %d not divisible by world %d", d->num_experts, world);
+  if (p2p && world > kEpMaxWorld)
+    return fail(TIDE_EUNSUPPORTED, "peer-memory EP supports world <= %d", kEpMaxWorld);
   if (d->num_experts / world < d->top_k && world > 1 && false)
     return fail(TIDE_EUNSUPPORTED, "fewer local experts than top_k");
   const int El = d->num_experts / world;
@@ -508,10 +509,6 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
   c->e0 = rank * El;
   const int N = c->maxN, k = c->k, R = c->rows_all;
   if (p2p) {  // one allocation holds everything the peers write (one IPC handle)
-    if (world > kEpMaxWorld) {
-      tide_ctx_destroy(c);
-      return fail(TIDE_EUNSUPPORTED, "peer-memory EP supports world <= %d", kEpMaxWorld);
-    }
     auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
     EpSymLayout& L = c->lay;
     L.x_all = 0;
@@ -519,7 +516,8 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     L.gates_all = up(L.topk_all + sizeof(int) * (size_t)R * k);
     L.recv = up(L.gates_all + sizeof(float) * (size_t)R * k);
     L.hits_all = up(L.recv + sizeof(float) * (size_t)R * c->H);
-    L.ctr = up(L.hits_all + sizeof(int) * (size_t)c->E);
+    L.ntok = up(L.hits_all + sizeof(int) * (size_t)c->E);
+    L.ctr = up(L.ntok + sizeof(int) * (size_t)kEpMaxWorld);
     L.total = up(L.ctr + sizeof(unsigned) * 8);
     c->p2p = true;
     ALLOC(c->sym, L.total);
@@ -830,6 +828,22 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.n_zero = 1 + c->max_entries;
   rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
                                        : nullptr;
+  rp.ep_P = 0;
+  rp.ep_rank = 0;
+  rp.zero_j = nullptr;
+  rp.n_zero_j = 0;
+  if (c->p2p) {  // peer-memory EP: the router dispatches (route.cuh)
+    rp.ep_P = c->world;
+    rp.ep_rank = c->rank;
+    for (int i = 0; i < kEpMaxWorld; ++i) rp.ep_base[i] = c->peers.base[i];
+    rp.ep_off_x = c->lay.x_all;
+    rp.ep_off_topk = c->lay.topk_all;
+    rp.ep_off_gates = c->lay.gates_all;
+    rp.ep_off_ntok = c->lay.ntok;
+    rp.ep_off_ctr = c->lay.ctr;
+    rp.zero_j = c->cnt_l;
+    rp.n_zero_j = c->El;
+  }
   // bf16 routers run phase 1 on the tensor cores (16 experts x 8 tokens per CTA);
   // TIDE_ROUTER_CC=1 forces the CUDA-core kernel (A/B measurement)
   if (c->bf16 && E % 16 == 0 && H % 256 == 0 && !getenv("TIDE_ROUTER_CC")) {
@@ -1206,23 +1220,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     CU_TRY(cudaMemsetAsync(c->topk + (size_t)N * k, 0xFF, sizeof(int) * (maxN - N) * k, st));
   // dispatch: every rank's tokens and routing to every rank (fixed counts, no host sync)
   const int nY = (H + 511) / 512;
-  if (c->p2p) {  // kernels store into the peers' symmetric regions (ep.cuh)
-    EpPushParams pp;
-    pp.peers = c->peers;
-    pp.lay = c->lay;
-    pp.x_in = static_cast<const uint4*>(c->x_in);
-    pp.topk = c->topk;
-    pp.gates = c->gates;
-    pp.par = c->cnt_par;
-    pp.rank = c->rank;
-    pp.maxN = maxN;
-    pp.N = N;
-    pp.k = k;
-    pp.row_u4 = (int)(c->eb * H / 16);
-    pp.cnt_l = c->cnt_l;
-    pp.El = El;
-    CU_TRY(launch_pdl(tide_ep_push_kernel, dim3(maxN, c->world), dim3(128), 0, st, pp));
-    c->launches++;
+  if (c->p2p) {
+    // dispatched by the route kernel above (route.cuh, ep_P > 0)
   } else {
     const ncclDataType_t xt = c->bf16 ? ncclBfloat16 : ncclFloat32;
     NC_TRY(ncclGroupStart());
@@ -1233,9 +1232,9 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[2], st));
   // local experts' token lists over all rows; their counts are the global hits (R-18)
-  if (c->p2p) {  // cnt_l was zeroed by the push kernel
+  if (c->p2p) {  // cnt_l was zeroed by the route kernel
     CU_TRY(launch_pdl(tide_ep_lists_p2p_kernel, dim3((R * k + 255) / 256), dim3(256), 0, st,
-                      c->sym, c->lay, (const int*)c->cnt_par, (unsigned)(c->world * maxN), R, k,
+                      c->sym, c->lay, (const int*)c->cnt_par, (unsigned)c->world, R, maxN, k,
                       c->e0, El, c->cnt_l, c->list_l, R, c->pslot_all));
   } else {
     CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));

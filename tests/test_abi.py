@@ -80,6 +80,18 @@ def test_argument_validation_without_device():
         assert rc == tide.TIDE_ECUDA and b"device" in L.tide_last_error()
     assert L.tide_moe_step(None, None, 0, None, None, None, 0, 1, 1, None, None, None, None,
                            None, None) == tide.TIDE_EINVAL
+    # peer-memory EP: arguments checked before any CUDA call
+    assert L.tide_ep_handle_bytes() == 64  # cudaIpcMemHandle_t
+    d16 = tide.make_desc(16, 2, 64, 64, 8)
+    assert L.tide_ctx_create_ep_p2p(ctypes.byref(d16), 0, 0, 16, ctypes.byref(h)) == \
+        tide.TIDE_EUNSUPPORTED  # world > 8
+    assert L.tide_ctx_create_ep_p2p(ctypes.byref(d16), 0, 0, 3, ctypes.byref(h)) == \
+        tide.TIDE_EUNSUPPORTED  # 16 experts not divisible by 3
+    assert L.tide_ctx_create_ep_p2p(ctypes.byref(d16), 0, 2, 2, ctypes.byref(h)) == tide.TIDE_EINVAL
+    assert L.tide_ctx_ep_connect(None, None, None) == tide.TIDE_EINVAL
+    assert L.tide_ctx_ep_export(None, None, None) == tide.TIDE_EINVAL
+    v = ctypes.c_int32()
+    assert L.tide_ctx_ep_error(None, ctypes.byref(v)) == tide.TIDE_EINVAL
 
 
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
