@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--interval", type=int, default=4)
     ap.add_argument("--layers", type=int, default=0, help="override the stack depth")
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--routing", choices=["calibrated", "uniform"], default="calibrated",
+                    help="calibrated temporal block routing (default) or the uniform iid stress "
+                         "case (alpha=0, a0=0, skew=0: the most unique experts per launch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -205,7 +208,8 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     # product API (tide_pack_expert); one context per layer (EP: this rank's E/P experts)
     layers = []
     for l in range(Lyr):
-        wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev)
+        wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev,
+                                           skew=0.0 if args.routing == "uniform" else g.SKEW)
         if ep:
             sl = slice(rank * El, (rank + 1) * El)
             wg, wu, wd = wg[sl].contiguous(), wu[sl].contiguous(), wd[sl].contiguous()
@@ -232,7 +236,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         else:
             ctx = tide.Context(desc, cap, 16, local_rank)
         layers.append(dict(router=wr, w=w, shared=shared, ctx=ctx,
-                           x=g.block_hidden_torch(s, seed, l, dev),
+                           x=g.block_hidden_torch(s, seed, l, dev, iid=args.routing == "uniform"),
                            pl=torch.zeros(El, dtype=torch.uint8, device=dev),
                            hits=torch.empty(E, dtype=torch.int32, device=dev),
                            out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
@@ -403,14 +407,30 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     e2e = None
     if not args.no_e2e:
         xh = [L["x"].cpu().pin_memory() for L in layers]
-        oh = torch.empty(N, H, dtype=torch.bfloat16).pin_memory()
-        xd = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+        oh = [torch.empty(N, H, dtype=torch.bfloat16).pin_memory() for _ in layers]
+        xd = [torch.empty(N, H, dtype=torch.bfloat16, device=dev) for _ in layers]
+        cs = torch.cuda.Stream(device=dev)  # copy stream: PCIe transfers overlap the layer-steps
+        ev_in = [torch.cuda.Event() for _ in layers]
+        ev_out = [torch.cuda.Event() for _ in layers]
 
         def e2e_step(t):
+            # every layer-step's input goes H2D on the copy stream (after the previous step's
+            # compute has consumed the buffers); each layer-step waits for its own input, and
+            # its output goes D2H on the copy stream while the next layer-step runs
+            ms = torch.cuda.current_stream()  # the capture stream under torch.cuda.graph
+            cs.wait_stream(ms)
+            with torch.cuda.stream(cs):
+                for li in range(len(layers)):
+                    xd[li].copy_(xh[li][t], non_blocking=True)
+                    ev_in[li].record(cs)
             for li, L in enumerate(layers):
-                xd.copy_(xh[li][t], non_blocking=True)
-                layer_step(L, t, x=xd)
-                oh.copy_(L["out"], non_blocking=True)
+                ms.wait_event(ev_in[li])
+                layer_step(L, t, x=xd[li])
+                ev_out[li].record(ms)
+                cs.wait_event(ev_out[li])
+                with torch.cuda.stream(cs):
+                    oh[li].copy_(L["out"], non_blocking=True)
+            ms.wait_stream(cs)
 
         e2e_graphs = None
         if graphs is not None:  # same launch mode as the headline: copies captured in the graphs
@@ -444,7 +464,8 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                "ms_per_step": ems / args.steps,
                "launch": "CUDA graph per block step (copies captured)" if e2e_graphs else "eager",
                "note": "tide_moe_step through the C ABI; per layer-step the block's hidden "
-                       "states are copied from pinned host and the output back"}
+                       "states are copied from pinned host and the output back, on a copy "
+                       "stream that overlaps the transfers with the layer-steps"}
         del e2e_graphs
 
     cpu = None
@@ -463,11 +484,14 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     res = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-           "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and "
-                   "calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)",
+           "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and " +
+                   ("calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)"
+                    if args.routing == "calibrated" else
+                    "uniform iid stress routing (alpha=0, a0=0, skew=0)"),
            "config": {"workload": workload_str(s, cap, args.interval), "layers": Lyr,
                       "tokens_per_layer_step": N, "num_experts": E, "top_k": k, "hidden": H,
                       "ffn": F, "capacity": cap, "interval": args.interval,
+                      "routing": args.routing,
                       "parallelism": (f"expert parallel x{world} (E/P = {El} experts per rank, "
                                       + ("peer-memory dispatch/combine kernels)" if args.p2p else
                                          "NCCL all-gather dispatch + all-to-all combine)")) if ep

@@ -291,7 +291,8 @@ def _uniform_torch_keys(keys, n: int, bound: float, device, out_dtype):
     return ((u * f32(2.0) - f32(1.0)) * f32(bound)).to(out_dtype)
 
 
-def layer_torch(shape: Shape, seed: int, layer: int, device, chunk: int = 32):
+def layer_torch(shape: Shape, seed: int, layer: int, device, chunk: int = 32,
+                skew: float = SKEW):
     """Device twin of layer_np: (wr [E,H], wg [E,F,H], wu [E,F,H], wd [E,H,F], shared|None),
     bit-identical to the host generator, generated `chunk` experts at a time."""
     import torch
@@ -307,4 +308,4 @@ def layer_torch(shape: Shape, seed: int, layer: int, device, chunk: int = 32):
             out[e0:e0 + len(es)] = _uniform_torch_keys(keys, n, math.sqrt(3.0 / fan), device,
                                                        dt).view(len(es), *out.shape[1:])
     shared = shared_torch(shape, seed, layer, device) if shape.shared_expert else None
-    return router_torch(shape, seed, layer, device), wg, wu, wd, shared
+    return router_torch(shape, seed, layer, device, skew=skew), wg, wu, wd, shared
