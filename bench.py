@@ -469,7 +469,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         del e2e_graphs
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
         cpu, _ = oracle_rate(s, args.seed, args.cpu_seconds, tokens=min(N, 32))
 
     io = None
