@@ -143,6 +143,8 @@ typedef struct {
                             start, phase 1 done, phase 2 start, phase 2 done (0 = n/a) */
   uint64_t* ffn_trace;   /* [8 * #SMs] per FFN CTA: entry, work list ready, producer done,
                             epilogue done (%globaltimer ns), items processed                */
+  uint64_t* ffn_item_trace; /* [4 * 64 * #SMs] per FFN CTA, its first 64 items: claim time,
+                            kind << 32 | entry, dependency met, last load issued (ns)      */
 } tide_step_debug;
 
 typedef struct tide_ctx tide_ctx;

@@ -66,6 +66,7 @@ struct FfnParams {
   float* y_out;
   int H, F, E, maxN, N, k, shared;
   unsigned long long* trace;  // debug: per CTA [entry, work list ready, producer done, epilogue done, items]
+  unsigned long long* itrace;  // debug: per CTA, 64 items x {claim, kind<<32|entry, dep met, issued}
   int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
   int shared_tok0;       // token id of its first row (0 single-device, rank*maxN under EP)
 };
@@ -226,6 +227,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       int it = 0;
       if (lane == 0) it = atomicAdd(p.sched, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
+      unsigned long long* itr = (p.itrace && n_items < 64)
+                                    ? p.itrace + 4 * (64 * (size_t)blockIdx.x + n_items) : nullptr;
+      if (itr && lane == 0) itr[0] = globaltimer_ns();
       FfnItem item;
       item.kind = -1;
       if (it < total) {
@@ -246,8 +250,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
       if (item.kind < 0) break;
       ++n_items;
+      if (itr && lane == 0) itr[1] = ((unsigned long long)item.kind << 32) | (unsigned)item.entry;
       const int nbox = (item.m + 15) >> 4;
       if (item.kind == 0) {
+        if (itr && lane == 0) itr[2] = globaltimer_ns();
         // token rows of this entry, gathered straight from x_in: lane i loads rows
         // 4i..4i+3 (rows past m repeat the last token; their MMA columns are discarded)
         const int ng = (item.m + 3) >> 2;
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
           }
         }
         __syncwarp();
+        if (itr && lane == 0) itr[2] = globaltimer_ns();
         fence_proxy_async_global();
         const CUtensorMap* ma = (item.flags & 1) ? &p.map_d_s : &p.map_d;
         const int rowd = item.slot * 3 * H + 2 * H + item.tile * kTileM;
@@ -316,6 +323,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
           if (++stage == kStages) { stage = 0; sphase ^= 1; }
         }
       }
+      if (itr && lane == 0) itr[3] = globaltimer_ns();
     }
     if (tr && lane == 0) { tr[2] = globaltimer_ns(); tr[4] = n_items; }
     // NEXT-3 cross-layer prefetch: this CTA has no more work, so its share of the next

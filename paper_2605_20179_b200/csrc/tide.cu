@@ -668,7 +668,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
                               int N, cudaStream_t st, bool ep_local = false,
                               unsigned long long* trace = nullptr, const int* par = nullptr,
-                              bool prefetch = false) {
+                              bool prefetch = false, unsigned long long* itrace = nullptr) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -707,6 +707,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.k = c->k;
   p.shared = (c->d.flags & TIDE_SHARED_EXPERT) ? 1 : 0;
   p.trace = trace;
+  p.itrace = itrace;
   p.shared_row0 = N * c->k;
   p.shared_tok0 = 0;
   if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
@@ -1109,7 +1110,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     s = launch_ffn(c, c->cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
                    c->ffn_ctrl + 1, N, st, false,
                    dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par,
-                   !pool_mode);
+                   !pool_mode,
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_item_trace) : nullptr);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));

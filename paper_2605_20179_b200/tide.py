@@ -64,7 +64,8 @@ class StepStats(ctypes.Structure):
 
 class StepDebug(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("topk_idx", "gates", "pos", "order", "offsets",
-                                                "logits", "route_trace", "ffn_trace")]
+                                                "logits", "route_trace", "ffn_trace",
+                                                "ffn_item_trace")]
 
 
 class PhaseTimes(ctypes.Structure):
@@ -269,7 +270,10 @@ class Context:
                      "route_trace": torch.zeros(4 * ((E + 7) // 8) * max(1, N),
                                                 dtype=torch.int64, device=dev),
                      "ffn_trace": torch.zeros(8 * torch.cuda.get_device_properties(dev).multi_processor_count,
-                                              dtype=torch.int64, device=dev)}
+                                              dtype=torch.int64, device=dev),
+                     "ffn_item_trace": torch.zeros(
+                         4 * 64 * torch.cuda.get_device_properties(dev).multi_processor_count,
+                         dtype=torch.int64, device=dev)}
             if debug == "trace":  # kernel timestamps only: no extra copies on the stream
                 dbg_t = {n: (v if n.endswith("_trace") else None) for n, v in dbg_t.items()}
             dbg = StepDebug(*((dbg_t[n].data_ptr() if dbg_t[n] is not None else None)
