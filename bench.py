@@ -517,18 +517,20 @@ def run_reference(args):
     import oracle
     s = shape_for(args)
     N = min(s.tokens, 8)
-    wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, 0, "cpu")
+    uni = args.routing == "uniform"
+    wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, 0, "cpu", skew=0.0 if uni else g.SKEW)
     to = g.torch_to_np
     L = oracle.Layer(to(wr), to(wg), to(wu), to(wd), tuple(to(a) for a in sh) if sh else None)
-    xs = g.block_hidden_np(s, args.seed, 0, steps=s.steps, tokens=N)
+    xs = g.block_hidden_np(s, args.seed, 0, steps=s.steps, tokens=N, iid=uni)
     E = s.num_experts
+    cap = args.capacity or E
     p = np.zeros(E, np.uint8)
     for i in range(args.warmup):
-        p = oracle.moe_step(L, xs[i % s.steps], s.top_k, p, i % s.steps, args.interval, E).placement
+        p = oracle.moe_step(L, xs[i % s.steps], s.top_k, p, i % s.steps, args.interval, cap).placement
     t0 = time.perf_counter()
     for i in range(args.steps):
         t = (args.warmup + i) % s.steps
-        p = oracle.moe_step(L, xs[t], s.top_k, p, t, args.interval, E).placement
+        p = oracle.moe_step(L, xs[t], s.top_k, p, t, args.interval, cap).placement
     el = time.perf_counter() - t0
     v = N * args.steps / el
     sample = (f"each step = one full layer-step (router..combine, fp64, single thread) of layer 0 "
@@ -537,7 +539,11 @@ def run_reference(args):
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * el / args.steps, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_str(s, E, args.interval) + f" [oracle sample: {N} tokens]"},
+            "config": {"workload": workload_str(s, cap, args.interval), "layers": s.layers,
+                       "tokens_per_layer_step": s.tokens, "num_experts": E, "top_k": s.top_k,
+                       "hidden": s.hidden, "ffn": s.ffn, "capacity": cap,
+                       "interval": args.interval, "routing": args.routing,
+                       "oracle_sample": f"{N} of {s.tokens} tokens of layer 0 per step"},
             "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
