@@ -119,9 +119,10 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
 //   tide_ep_lists_kernel    (p2p) waits until all P sources have arrived
 //   tide_ep_partial_kernel  (p2p) stores each source row's partial straight into the
 //                           source rank's recv[rank][n] (and the local experts' counts into
-//                           its hits_all), then arrives on its combine counter
-//   tide_ep_final_kernel    (p2p) waits for all P*maxN*ceil(H/512) partial CTAs, then the
-//                           same rank-order sum as the NCCL path (bitwise identical)
+//                           its hits_all); the last CTA per source arrives on its combine
+//                           counter (one arrival per source rank)
+//   tide_ep_final_kernel    (p2p) waits for the P arrivals, then the same rank-order sum as
+//                           the NCCL path (bitwise identical)
 // Counters are double-buffered by the step parity word the route kernel flips; the lists
 // kernel of a step zeroes the other parity's counters (their last readers finished a step
 // ago; their next writers need this step's partials first).  A waiting CTA gives up after
@@ -173,15 +174,6 @@ __device__ __forceinline__ bool ep_wait_all(const unsigned* ctr, unsigned target
   return s_ok != 0;
 }
 
-// Every thread's stores of this CTA become visible to the destination GPU before the arrival.
-__device__ __forceinline__ void ep_arrive(unsigned* ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    red_release_sys_add_u32(ctr, 1u);
-  }
-}
-
 // p2p variant of tide_ep_lists_kernel: wait for the P sources' dispatch first; rows past a
 // source's token count hold stale routing and are skipped (pslot -1).
 __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
@@ -218,8 +210,8 @@ __global__ void __launch_bounds__(128) tide_ep_partial_p2p_kernel(
     EpPeers peers, EpSymLayout lay, const float* __restrict__ y,
     const int* __restrict__ topk_all, const float* __restrict__ gates_all,
     const int* __restrict__ pslot_all, const int* __restrict__ off_l,
-    const int* __restrict__ cnt_l, const int* par_word, int rank, int maxN, int k, int H,
-    int e0, int El) {
+    const int* __restrict__ cnt_l, const int* par_word, unsigned* part_cnt, int rank, int maxN,
+    int k, int H, int e0, int El) {
   pdl_wait();
   pdl_trigger();
   const int row = blockIdx.x, lane = threadIdx.x & 31;
@@ -256,8 +248,19 @@ __global__ void __launch_bounds__(128) tide_ep_partial_p2p_kernel(
     int* hits = reinterpret_cast<int*>(b + lay.hits_all) + e0;
     for (int i = threadIdx.x; i < El; i += blockDim.x) hits[i] = __ldcg(cnt_l + i);
   }
+  // arrive: gpu-scope count per destination; the destination's last CTA publishes all of
+  // them with one system-scope fence and a single release on the destination's counter
   const int par = __ldcg(par_word);
-  ep_arrive(reinterpret_cast<unsigned*>(b + lay.ctr) + 2 + par);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned per_dst = (unsigned)maxN * gridDim.y;
+    if (atomicAdd(part_cnt + src, 1u) == per_dst - 1) {
+      part_cnt[src] = 0u;
+      __threadfence_system();
+      red_release_sys_add_u32(reinterpret_cast<unsigned*>(b + lay.ctr) + 2 + par, 1u);
+    }
+  }
 }
 
 // p2p variant of tide_ep_final_kernel: grid (max(N,1), ceil(H/512)).  CTA (0,0) also

@@ -254,8 +254,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   __syncthreads();
   if (tid == 0) {
     if (tr) tr[1] = globaltimer_ns();
-    if (p.ep_P) __threadfence_system();  // this CTA's x stores to the peers (route_ep_push_x)
-    __threadfence();
+    __threadfence();  // (EP: the grid's last CTA publishes everything at system scope)
     s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
@@ -291,13 +290,13 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
-    if (p.ep_P) __threadfence_system();
     __threadfence();
     if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
       __threadfence();
-      if (p.ep_P) {  // every group's stores precede this point (g_done chain): arrive
+      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
+                     // g_cnt / g_done chains; one system-scope fence publishes them: arrive
         for (int dst = 0; dst < p.ep_P; ++dst)
           reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
         __threadfence_system();

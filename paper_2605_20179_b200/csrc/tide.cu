@@ -190,6 +190,7 @@ struct tide_ctx {
   EpSymLayout lay{};
   EpPeers peers{};
   std::vector<void*> ipc_opened;  // peers' regions opened with cudaIpcOpenMemHandle
+  unsigned* part_cnt = nullptr;   // [kEpMaxWorld] partial-kernel CTAs per destination (self-resetting)
 
   // per-phase timing (tide_ctx_set_timing)
   bool timing = false;
@@ -343,7 +344,8 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n};
+                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n,
+                 c->part_cnt};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -521,6 +523,7 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     L.total = up(L.ctr + sizeof(unsigned) * 8);
     c->p2p = true;
     ALLOC(c->sym, L.total);
+    ALLOC(c->part_cnt, sizeof(unsigned) * kEpMaxWorld);
     c->x_all = c->sym + L.x_all;
     c->topk_all = reinterpret_cast<int*>(c->sym + L.topk_all);
     c->gates_all = reinterpret_cast<float*>(c->sym + L.gates_all);
@@ -1265,11 +1268,11 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
                       (const float*)c->y_perm, (const int*)c->topk_all,
                       (const float*)c->gates_all, (const int*)c->pslot_all,
                       (const int*)c->off_l, (const int*)c->cnt_l, (const int*)c->cnt_par,
-                      c->rank, maxN, k, H, c->e0, El));
+                      c->part_cnt, c->rank, maxN, k, H, c->e0, El));
     c->launches++;
     if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
     const dim3 grid(std::max(N, 1), nY);
-    const unsigned tgt = (unsigned)(c->world * maxN * nY);
+    const unsigned tgt = (unsigned)c->world;  // one arrival per source rank
     if (c->bf16)
       CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<__nv_bfloat16>, grid, dim3(128), 0, st, c->sym,
                         c->lay, (const int*)c->cnt_par, tgt, (const float*)c->y_perm,
