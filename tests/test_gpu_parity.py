@@ -273,4 +273,3 @@ def test_router_logit_error(shape_name, tokens):
     torch.cuda.synchronize()
     err = np.abs(r.debug["logits"].cpu().numpy().astype(np.float64) - ref).max()
     assert err < 6e-7, f"max |logit - fp64| = {err:.3e}"
-
