@@ -117,12 +117,13 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
 //                           topk_all / gates_all / ntok at [rank*maxN + n]; one arrival per
 //                           source rank on each destination's dispatch counter
 //   tide_ep_lists_kernel    (p2p) waits until all P sources have arrived
-//   tide_ep_partial_kernel  (p2p) stores each source row's partial straight into the
-//                           source rank's recv[rank][n] (and the local experts' counts into
-//                           its hits_all); the last CTA per source arrives on its combine
-//                           counter (one arrival per source rank)
-//   tide_ep_final_kernel    (p2p) waits for the P arrivals, then the same rank-order sum as
-//                           the NCCL path (bitwise identical)
+//   tide_ffn_kernel<T,true> (p2p) the phase-2 epilogue stores each routed pair's y row
+//                           straight into the owning rank's ypair[n*k + j]; the grid's last
+//                           CTA delivers the local experts' counts into every hits_all and
+//                           arrives once per rank on its combine counter (ffn.cuh)
+//   tide_ep_final_kernel    (p2p) waits for the P arrivals, then exactly the single-device
+//                           combine: out[n] = sum_j g[n,j] y[n,j] in slot order (+ shared),
+//                           so the EP output equals the single-device output bit for bit
 // Counters are double-buffered by the step parity word the route kernel flips; the lists
 // kernel of a step zeroes the other parity's counters (their last readers finished a step
 // ago; their next writers need this step's partials first).  A waiting CTA gives up after
@@ -137,7 +138,8 @@ struct EpPeers {
 static_assert(kEpMaxWorld == kRouteEpMax, "route.cuh and ep.cuh disagree on the max world");
 
 struct EpSymLayout {  // byte offsets inside a rank's symmetric region
-  size_t x_all, topk_all, gates_all, recv, hits_all, ntok, ctr, total;
+  size_t x_all, topk_all, gates_all, ypair, hits_all, ntok, ctr, total;
+  // ypair: [maxN * k][H] fp32, y of this rank's pair (n, j) written by its expert's owner
   // ntok: [P] tokens each source rank dispatched this step (rows >= ntok[src] are stale)
   // ctr: [0..1] dispatch arrivals by parity, [2..3] combine arrivals by parity, [4] error
 };
@@ -179,7 +181,7 @@ __device__ __forceinline__ bool ep_wait_all(const unsigned* ctr, unsigned target
 __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
     char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int maxN, int k,
     int e0, int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
-    int* __restrict__ pslot_all) {
+    int* __restrict__ pslot_all, unsigned* __restrict__ dst_l) {
   pdl_wait();  // this rank's route kernel (and its cnt_l zeroing) is complete
   unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
   const int par = __ldcg(par_word);
@@ -197,84 +199,29 @@ __global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
   if (e >= e0 && e < e0 + El) {
     const int s = atomicAdd(&cnt_l[e - e0], 1);
     list_l[(size_t)(e - e0) * list_stride + s] = q / k;
+    // where the FFN epilogue stores this pair's y: source rank << 28 | its row n*k + j there
+    dst_l[(size_t)(e - e0) * list_stride + s] =
+        ((unsigned)src << 28) | (unsigned)((row - src * maxN) * k + (q - row * k));
     pslot_all[q] = s;
   } else {
     pslot_all[q] = -1;
   }
 }
 
-// p2p variant of tide_ep_partial_kernel: grid (P*maxN, ceil(H/512)); row's partial goes to
-// the source rank (row / maxN) at recv[rank][row % maxN]; the first row CTA of each source
-// also delivers this rank's local-expert counts into the source's hits_all[e0 .. e0+El).
-__global__ void __launch_bounds__(128) tide_ep_partial_p2p_kernel(
-    EpPeers peers, EpSymLayout lay, const float* __restrict__ y,
-    const int* __restrict__ topk_all, const float* __restrict__ gates_all,
-    const int* __restrict__ pslot_all, const int* __restrict__ off_l,
-    const int* __restrict__ cnt_l, const int* par_word, unsigned* part_cnt, int rank, int maxN,
-    int k, int H, int e0, int El) {
-  pdl_wait();
-  pdl_trigger();
-  const int row = blockIdx.x, lane = threadIdx.x & 31;
-  const int src = row / maxN, n = row - src * maxN;
-  char* b = peers.base[src];
-  const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  int r_j = -1;
-  float g_j = 0.f;
-  if (lane < k) {  // pslot >= 0 iff the pair is live and routed to a local expert
-    const int q = row * k + lane;
-    const int sl = __ldcg(pslot_all + q);
-    if (sl >= 0) {
-      r_j = __ldcg(off_l + (__ldcg(topk_all + q) - e0)) + sl;
-      g_j = __ldcg(gates_all + q);
-    }
-  }
-  const bool valid = c < H;
-  const int cc = valid ? c : 0;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = 0; j < k; ++j) {
-    const int r = __shfl_sync(0xffffffffu, r_j, j);
-    const float g = __shfl_sync(0xffffffffu, g_j, j);
-    if (r < 0) continue;
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)r * H + cc));
-    acc.x = fmaf(g, v.x, acc.x);
-    acc.y = fmaf(g, v.y, acc.y);
-    acc.z = fmaf(g, v.z, acc.z);
-    acc.w = fmaf(g, v.w, acc.w);
-  }
-  if (valid)
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(b + lay.recv) +
-                               ((size_t)rank * maxN + n) * H + c) = acc;
-  if (n == 0 && blockIdx.y == 0) {
-    int* hits = reinterpret_cast<int*>(b + lay.hits_all) + e0;
-    for (int i = threadIdx.x; i < El; i += blockDim.x) hits[i] = __ldcg(cnt_l + i);
-  }
-  // arrive: gpu-scope count per destination; the destination's last CTA publishes all of
-  // them with one system-scope fence and a single release on the destination's counter
-  const int par = __ldcg(par_word);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned per_dst = (unsigned)maxN * gridDim.y;
-    if (atomicAdd(part_cnt + src, 1u) == per_dst - 1) {
-      part_cnt[src] = 0u;
-      __threadfence_system();
-      red_release_sys_add_u32(reinterpret_cast<unsigned*>(b + lay.ctr) + 2 + par, 1u);
-    }
-  }
-}
-
-// p2p variant of tide_ep_final_kernel: grid (max(N,1), ceil(H/512)).  CTA (0,0) also
-// copies the global hits.
+// p2p variant of tide_ep_final_kernel: grid (max(N,1), ceil(H/512)), 128 threads x 4 columns.
+// Waits for the P ranks' FFN arrivals, then the single-device combine's arithmetic on the
+// pairs' y rows in ypair (slot order, fp32 fma, + shared expert, one rounding).  CTA (0,0)
+// also copies the global hits.
 template <typename T>
 __global__ void __launch_bounds__(128) tide_ep_final_p2p_kernel(
-    char* sym, EpSymLayout lay, const int* par_word, unsigned target, const float* __restrict__ y,
-    T* __restrict__ out, int32_t* __restrict__ hit_counts, int E, int N, int P, int maxN, int H,
-    int shared_row0) {
+    char* sym, EpSymLayout lay, const int* par_word, unsigned target, const float* __restrict__ gates,
+    const float* __restrict__ y, T* __restrict__ out, int32_t* __restrict__ hit_counts, int E,
+    int N, int k, int H, int shared_row0) {
   pdl_wait();
   pdl_trigger();
   unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
   const int par = __ldcg(par_word);
-  const int n = blockIdx.x;
+  const int n = blockIdx.x, lane = threadIdx.x & 31;
   if (n >= N && !(n == 0 && blockIdx.y == 0)) return;
   if (!ep_wait_all(ctr + 2 + par, target, ctr + 4)) return;
   if (n == 0 && blockIdx.y == 0) {
@@ -282,17 +229,23 @@ __global__ void __launch_bounds__(128) tide_ep_final_p2p_kernel(
     for (int i = threadIdx.x; i < E; i += blockDim.x) hit_counts[i] = __ldcg(hits + i);
   }
   if (n >= N) return;
-  const float* recv = reinterpret_cast<const float*>(sym + lay.recv);
+  const float* yp = reinterpret_cast<const float*>(sym + lay.ypair);
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  if (c >= H) return;
-  float4 acc = __ldcg(reinterpret_cast<const float4*>(recv + (size_t)n * H + c));
-  for (int p = 1; p < P; ++p) {  // rank order (same arithmetic as tide_ep_final_kernel)
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(recv + ((size_t)p * maxN + n) * H + c));
-    acc.x += v.x;
-    acc.y += v.y;
-    acc.z += v.z;
-    acc.w += v.w;
+  float g_j = 0.f;
+  if (lane < k) g_j = __ldcg(gates + (size_t)n * k + lane);
+  const bool valid = c < H;
+  const int cc = valid ? c : 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+  for (int j = 0; j < k; ++j) {
+    const float g = __shfl_sync(0xffffffffu, g_j, j);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(yp + ((size_t)n * k + j) * H + cc));
+    acc.x = fmaf(g, v.x, acc.x);
+    acc.y = fmaf(g, v.y, acc.y);
+    acc.z = fmaf(g, v.z, acc.z);
+    acc.w = fmaf(g, v.w, acc.w);
   }
+  if (!valid) return;
   if (shared_row0 >= 0) {
     const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(shared_row0 + n) * H + c));
     acc.x += v.x;

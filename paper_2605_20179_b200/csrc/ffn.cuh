@@ -67,6 +67,18 @@ struct FfnParams {
   int H, F, E, maxN, N, k, shared;
   unsigned long long* trace;  // debug: per CTA [entry, work list ready, producer done, epilogue done, items]
   unsigned long long* itrace;  // debug: per CTA, 64 items x {claim, kind<<32|entry, dep met, issued}
+  // Peer-memory EP (tide_ffn_kernel<T, true>): the phase-2 epilogue stores each routed pair's
+  // y row straight into the owning rank's ypair[n*k + j] over peer memory -- the combine's
+  // exchange fused into the GEMM epilogue; the grid's last CTA then delivers the local
+  // experts' counts into every rank's hits_all and arrives once on each rank's combine
+  // counter (one system-scope fence per launch).  Shared-expert rows stay local (y_out).
+  int ep_P, ep_e0, ep_El;
+  const unsigned* ep_dst; // [El][rows_all] per list slot: owner rank << 28 | pair row n*k + j
+  const int* ep_cnt_l;    // [El] local experts' counts (global hits of those experts)
+  const int* ep_par;      // step parity word (flipped by the route kernel)
+  int* ep_done;           // grid arrival counter (zeroed by the route kernel)
+  char* ep_base[8];       // symmetric regions of every rank
+  size_t ep_off_ypair, ep_off_hits, ep_off_ctr;
   int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
   int shared_tok0;       // token id of its first row (0 single-device, rank*maxN under EP)
 };
@@ -76,7 +88,7 @@ struct FfnItem {
   int tile, slot, off, m, flags, entry, tokbase;
 };
 
-template <typename T>
+template <typename T, bool EP>
 __global__ void __launch_bounds__(kFfnThreads, 1)
     tide_ffn_kernel(const __grid_constant__ FfnParams p) {
   constexpr bool kTF32 = std::is_same<T, float>::value;
@@ -430,6 +442,23 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
             }
           }
         }
+      } else if (EP && !(item.flags & 2)) {  // EP: y of pair (n, j) -> owner's ypair[n*k + j]
+        const int h = item.tile * kTileM + row;
+        for (int c0 = 0; c0 < item.m; c0 += 16) {
+          float v[16];
+          unsigned d[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)  // same address in every thread: broadcast loads
+            d[i] = c0 + i < item.m ? __ldg(p.ep_dst + item.tokbase + c0 + i) : 0u;
+          tmem_ld16(tbase + c0, v);
+          if (h < H) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < item.m)
+                reinterpret_cast<float*>(p.ep_base[d[i] >> 28] + p.ep_off_ypair)
+                    [(size_t)(d[i] & 0x0FFFFFFFu) * H + h] = v[i];
+          }
+        }
       } else {
         const int h = item.tile * kTileM + row;
         float* ycol = p.y_out + h;
@@ -460,6 +489,30 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if constexpr (EP) {  // every CTA's peer stores precede its gpu-scope arrival
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(p.ep_done, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // the grid's last CTA: counts to every rank, one system fence, arrive
+      __threadfence();
+      for (int i = threadIdx.x; i < p.ep_P * p.ep_El; i += blockDim.x) {
+        const int dst = i / p.ep_El, e = i - dst * p.ep_El;
+        reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_hits)[p.ep_e0 + e] = __ldcg(p.ep_cnt_l + e);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int par = __ldcg(p.ep_par);
+        __threadfence_system();
+        for (int dst = 0; dst < p.ep_P; ++dst)
+          asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(
+                           reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par),
+                       "r"(1u) : "memory");
+      }
+    }
   }
 }
 

@@ -138,7 +138,8 @@ struct tide_ctx {
   void* x_in = nullptr;      // [maxN, H] copy of the block's hidden states (gather4 source)
   void* h_perm = nullptr;    // [max_rows, F]
   float* y_perm = nullptr;   // [max_rows, H]
-  int* ffn_ctrl = nullptr;   // [1 + max_entries]: scheduler counter + per-entry done counters
+  int* ffn_ctrl = nullptr;   // [2 + max_entries]: scheduler counter, per-entry done counters,
+                             // grid arrival counter (peer-memory EP)
   RouteInfo* info = nullptr; // + hits[E] + placement[E]
   size_t info_bytes = 0;
   int* slot_of_dev = nullptr;
@@ -190,7 +191,7 @@ struct tide_ctx {
   EpSymLayout lay{};
   EpPeers peers{};
   std::vector<void*> ipc_opened;  // peers' regions opened with cudaIpcOpenMemHandle
-  unsigned* part_cnt = nullptr;   // [kEpMaxWorld] partial-kernel CTAs per destination (self-resetting)
+  unsigned* dst_l = nullptr;      // [El, rows_all] owner rank << 28 | pair row of each list slot (p2p)
 
   // per-phase timing (tide_ctx_set_timing)
   bool timing = false;
@@ -267,17 +268,16 @@ static void preload_ep_p2p_kernels(const tide_ctx* c) {
   }
   if (c->bf16) {
     TOUCH_ROUTE(__nv_bfloat16)
-    touch(tide_ffn_kernel<__nv_bfloat16>);
+    touch(tide_ffn_kernel<__nv_bfloat16, true>);
     touch(tide_ep_final_p2p_kernel<__nv_bfloat16>);
   } else {
     TOUCH_ROUTE(float)
-    touch(tide_ffn_kernel<float>);
+    touch(tide_ffn_kernel<float, true>);
     touch(tide_ep_final_p2p_kernel<float>);
   }
 #undef TOUCH_ROUTE
   touch(tide_book_kernel);
   touch(tide_ep_lists_p2p_kernel);
-  touch(tide_ep_partial_p2p_kernel);
 }
 
 extern "C" {
@@ -345,7 +345,7 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
                  c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n,
-                 c->part_cnt};
+                 c->dst_l};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {c->h_info, c->h_entries2, c->h_ctrl2, c->h_slot_of};
@@ -432,7 +432,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->x_in, c->eb * (size_t)N * c->H);
   ALLOC(c->h_perm, c->eb * (size_t)c->max_rows * c->F);
   ALLOC(c->y_perm, sizeof(float) * (size_t)c->max_rows * c->H);
-  ALLOC(c->ffn_ctrl, sizeof(int) * (1 + c->max_entries));
+  ALLOC(c->ffn_ctrl, sizeof(int) * (2 + c->max_entries));
   c->info_bytes = sizeof(RouteInfo) + sizeof(int) * E + E;
   ALLOC(c->info, c->info_bytes);
   ALLOC(c->slot_of_dev, sizeof(int) * E);
@@ -452,12 +452,17 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
     tide_ctx_destroy(c);
     return fail(TIDE_ECUDA, "%s", m.c_str());
   }
-  if (c->bf16)
-    cudaFuncSetAttribute(tide_ffn_kernel<__nv_bfloat16>,
+  if (c->bf16) {
+    cudaFuncSetAttribute(tide_ffn_kernel<__nv_bfloat16, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kFfnSmemBytes);
-  else
-    cudaFuncSetAttribute(tide_ffn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tide_ffn_kernel<__nv_bfloat16, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kFfnSmemBytes);
+  } else {
+    cudaFuncSetAttribute(tide_ffn_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kFfnSmemBytes);
+    cudaFuncSetAttribute(tide_ffn_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kFfnSmemBytes);
+  }
   cudaFuncSetAttribute(tide_book_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(int) * 6 * E));
   cudaError_t e = cudaDeviceSynchronize();
@@ -516,18 +521,17 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     L.x_all = 0;
     L.topk_all = up(L.x_all + c->eb * (size_t)R * c->H);
     L.gates_all = up(L.topk_all + sizeof(int) * (size_t)R * k);
-    L.recv = up(L.gates_all + sizeof(float) * (size_t)R * k);
-    L.hits_all = up(L.recv + sizeof(float) * (size_t)R * c->H);
+    L.ypair = up(L.gates_all + sizeof(float) * (size_t)R * k);
+    L.hits_all = up(L.ypair + sizeof(float) * (size_t)N * k * c->H);
     L.ntok = up(L.hits_all + sizeof(int) * (size_t)c->E);
     L.ctr = up(L.ntok + sizeof(int) * (size_t)kEpMaxWorld);
     L.total = up(L.ctr + sizeof(unsigned) * 8);
     c->p2p = true;
     ALLOC(c->sym, L.total);
-    ALLOC(c->part_cnt, sizeof(unsigned) * kEpMaxWorld);
+    ALLOC(c->dst_l, sizeof(unsigned) * (size_t)El * R);
     c->x_all = c->sym + L.x_all;
     c->topk_all = reinterpret_cast<int*>(c->sym + L.topk_all);
     c->gates_all = reinterpret_cast<float*>(c->sym + L.gates_all);
-    c->recv = reinterpret_cast<float*>(c->sym + L.recv);
     c->peers.base[rank] = c->sym;
     c->connected = world == 1;
   } else {
@@ -711,6 +715,28 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.shared = (c->d.flags & TIDE_SHARED_EXPERT) ? 1 : 0;
   p.trace = trace;
   p.itrace = itrace;
+  p.ep_P = 0;
+  p.ep_e0 = 0;
+  p.ep_El = 0;
+  p.ep_dst = nullptr;
+  p.ep_cnt_l = nullptr;
+  p.ep_par = nullptr;
+  p.ep_done = nullptr;
+  p.ep_off_ypair = p.ep_off_hits = p.ep_off_ctr = 0;
+  for (int i = 0; i < kEpMaxWorld; ++i) p.ep_base[i] = nullptr;
+  if (ep_local && c->p2p) {  // fused owner scatter of the combine (ffn.cuh)
+    p.ep_P = c->world;
+    p.ep_e0 = c->e0;
+    p.ep_El = c->El;
+    p.ep_dst = c->dst_l;
+    p.ep_cnt_l = c->cnt_l;
+    p.ep_par = c->cnt_par;
+    p.ep_done = c->ffn_ctrl + 1 + c->max_entries;
+    for (int i = 0; i < kEpMaxWorld; ++i) p.ep_base[i] = c->peers.base[i];
+    p.ep_off_ypair = c->lay.ypair;
+    p.ep_off_hits = c->lay.hits_all;
+    p.ep_off_ctr = c->lay.ctr;
+  }
   p.shared_row0 = N * c->k;
   p.shared_tok0 = 0;
   if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
@@ -722,12 +748,14 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
     p.shared_row0 = c->rows_all * c->k;
     p.shared_tok0 = c->rank * c->maxN;
   }
+  const bool ep_scatter = p.ep_P > 0;
   if (c->bf16)
-    CU_TRY(launch_pdl(tide_ffn_kernel<__nv_bfloat16>, dim3(c->num_sms), dim3(kFfnThreads),
-                      kFfnSmemBytes, st, p));
+    CU_TRY(launch_pdl(ep_scatter ? tide_ffn_kernel<__nv_bfloat16, true>
+                                 : tide_ffn_kernel<__nv_bfloat16, false>,
+                      dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes, st, p));
   else
-    CU_TRY(launch_pdl(tide_ffn_kernel<float>, dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes,
-                      st, p));
+    CU_TRY(launch_pdl(ep_scatter ? tide_ffn_kernel<float, true> : tide_ffn_kernel<float, false>,
+                      dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes, st, p));
   c->launches++;
   c->ffn_launches++;
   return TIDE_OK;
@@ -829,7 +857,7 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.mask = c->mask;
   rp.g_cnt = c->g_cnt;
   rp.zero_i = c->ffn_ctrl;
-  rp.n_zero = 1 + c->max_entries;
+  rp.n_zero = 2 + c->max_entries;
   rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
                                        : nullptr;
   rp.ep_P = 0;
@@ -1240,7 +1268,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   if (c->p2p) {  // cnt_l was zeroed by the route kernel
     CU_TRY(launch_pdl(tide_ep_lists_p2p_kernel, dim3((R * k + 255) / 256), dim3(256), 0, st,
                       c->sym, c->lay, (const int*)c->cnt_par, (unsigned)c->world, R, maxN, k,
-                      c->e0, El, c->cnt_l, c->list_l, R, c->pslot_all));
+                      c->e0, El, c->cnt_l, c->list_l, R, c->pslot_all, c->dst_l));
   } else {
     CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
     tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El,
@@ -1263,25 +1291,20 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
   // a10: per-source partial sums, exchange, rank-order sum
   const int srow = shared ? R * k : -1;
-  if (c->p2p) {
-    CU_TRY(launch_pdl(tide_ep_partial_p2p_kernel, dim3(R, nY), dim3(128), 0, st, c->peers, c->lay,
-                      (const float*)c->y_perm, (const int*)c->topk_all,
-                      (const float*)c->gates_all, (const int*)c->pslot_all,
-                      (const int*)c->off_l, (const int*)c->cnt_l, (const int*)c->cnt_par,
-                      c->part_cnt, c->rank, maxN, k, H, c->e0, El));
-    c->launches++;
+  if (c->p2p) {  // the FFN stored every pair's y at its owner and arrived (ffn.cuh)
     if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
     const dim3 grid(std::max(N, 1), nY);
-    const unsigned tgt = (unsigned)c->world;  // one arrival per source rank
+    const unsigned tgt = (unsigned)c->world;  // one FFN arrival per rank
     if (c->bf16)
       CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<__nv_bfloat16>, grid, dim3(128), 0, st, c->sym,
-                        c->lay, (const int*)c->cnt_par, tgt, (const float*)c->y_perm,
-                        static_cast<__nv_bfloat16*>(out), hit_counts, c->E, N, c->world, maxN, H,
-                        srow));
+                        c->lay, (const int*)c->cnt_par, tgt, (const float*)c->gates,
+                        (const float*)c->y_perm, static_cast<__nv_bfloat16*>(out), hit_counts,
+                        c->E, N, k, H, srow));
     else
       CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<float>, grid, dim3(128), 0, st, c->sym, c->lay,
-                        (const int*)c->cnt_par, tgt, (const float*)c->y_perm,
-                        static_cast<float*>(out), hit_counts, c->E, N, c->world, maxN, H, srow));
+                        (const int*)c->cnt_par, tgt, (const float*)c->gates,
+                        (const float*)c->y_perm, static_cast<float*>(out), hit_counts, c->E, N,
+                        k, H, srow));
     c->launches++;
   } else {
     CU_TRY(launch_pdl(tide_ep_partial_kernel, dim3(R, nY), dim3(128), 0, st,

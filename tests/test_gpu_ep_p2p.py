@@ -8,7 +8,8 @@ combine done by the kernels over peer memory instead of NCCL (include/tide.h, ep
   the peers' symmetric regions, release/acquire counters at system scope, parity
   double-buffering); checked against the oracle's EP emulation (O11):
   global hits and per-rank placements exact, outputs within the north-star tolerance,
-  over several steps with ragged per-rank token counts, and bitwise repeatable.
+  and bitwise equal to the single-device step on all ranks' tokens, over several steps
+  with ragged per-rank token counts; bitwise repeatable.
 - world = 2 across two PROCESSES on one B200, peers mapped with CUDA IPC
   (tide_ctx_ep_export / connect with `handles`), the multi-process setup path.
 """
@@ -101,8 +102,8 @@ def _emulated(world, seed, tokens, steps, interval, cap_r):
                                                 out=outs_buf[r], hit_counts=hits_buf[r],
                                                 placement_out=pl[r]))
         torch.cuda.synchronize()
-        res.append([(to_np_f64(o.out), o.hit_counts.cpu().numpy(), o.placement.cpu().numpy())
-                    for o in outs])
+        res.append([(to_np_f64(o.out), o.hit_counts.cpu().numpy(), o.placement.cpu().numpy(),
+                     o.out.view(torch.int16).cpu().numpy()) for o in outs])
     for c in ctxs:
         assert c.error() == 0, "peer-memory wait timed out"
     return layer, xs, res
@@ -110,23 +111,35 @@ def _emulated(world, seed, tokens, steps, interval, cap_r):
 
 @pytest.mark.parametrize("world,tokens,cap_r", [(2, (24, 17), 10), (4, (24, 5, 0, 13), 3)])
 def test_p2p_emulated_world_matches_oracle_ep(world, tokens, cap_r):
+    """Per rank: hits and placement' exact vs the oracle's EP emulation (O11), outputs within
+    2e-2 of it, and every output bit equal to the single-device step on all ranks' tokens
+    (the combine runs the single-device arithmetic on the pairs' y rows)."""
+    from paper_2605_20179_b200 import tide
     steps, interval = 4, 2
     layer, xs, res = _emulated(world, 61, tokens, steps, interval, cap_r)
     E, k = SHAPE.num_experts, SHAPE.top_k
     El = E // world
     ol = layer.oracle_layer()
     p_in = np.zeros(E, np.uint8)
+    single = tide.Context(desc_for(SHAPE, max_tokens=sum(tokens)), E)
+    p1 = torch.zeros(E, dtype=torch.uint8, device="cuda")
     for t in range(steps):
         x_cat = np.concatenate([xs[r][t % SHAPE.steps][:tokens[r]] for r in range(world)])
         _, hits, pout, out = oracle.ep_step(ol, world, x_cat, k, p_in, t, interval, cap_r)
+        one = single.moe_step(g.np_to_torch(x_cat, "cuda"), layer.router, **layer.weights(),
+                              placement=p1, step=t, interval=interval, placement_out=p1)
+        torch.cuda.synchronize()
+        one_out = one.out.view(torch.int16).cpu().numpy()
         row = 0
         for r in range(world):
-            o, h, p = res[t][r]
+            o, h, p, _ = res[t][r]
             assert (h == hits).all(), (t, r)
             assert (p == pout[r * El:(r + 1) * El]).all(), (t, r)
             if tokens[r]:
                 err = rel_err(o, out[row:row + tokens[r]])
                 assert err < OUT_TOL, (t, r, err)
+                ob = res[t][r][3]
+                assert np.array_equal(ob, one_out[row:row + tokens[r]]), (t, r)
             row += tokens[r]
         p_in = pout
 
@@ -135,7 +148,7 @@ def test_p2p_emulated_repeat_bitwise():
     _, _, a = _emulated(2, 71, (24, 24), 3, 1, 16)
     _, _, b = _emulated(2, 71, (24, 24), 3, 1, 16)
     for ra, rb in zip(a, b):
-        for (oa, ha, pa), (ob, hb, pb) in zip(ra, rb):
+        for (oa, ha, pa, _), (ob, hb, pb, _) in zip(ra, rb):
             assert np.array_equal(oa, ob) and np.array_equal(ha, hb) and np.array_equal(pa, pb)
 
 
