@@ -185,6 +185,16 @@ def h2d_peak_gbs(dev, mb: int = 256, reps: int = 5) -> float:
     return best
 
 
+def max_over_ranks(v: float, world: int, dev) -> float:
+    """MAX over ranks of a device-timed value (NCCL: device tensor; gloo test mode: host)."""
+    if world == 1:
+        return v
+    gloo = torch.distributed.get_backend() == "gloo"
+    tm = torch.tensor([v], device="cpu" if gloo else dev)
+    torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+    return float(tm.item())
+
+
 def run_tide(args, rank: int, world: int, local_rank: int):
     from paper_2605_20179_b200 import tide
     torch.cuda.set_device(local_rank)
@@ -304,9 +314,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1)
         if world > 1:
-            tm = torch.tensor([t], device=dev)
-            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
-            t = float(tm.item())
+            t = max_over_ranks(t, world, dev)
         ph = [L["ctx"].timing() for L in layers] if phase_timing else None
         for L in layers:
             L["ctx"].set_timing(False)
@@ -456,9 +464,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if world > 1:
-            tm = torch.tensor([ems], device=dev)
-            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
-            ems = float(tm.item())
+            ems = max_over_ranks(ems, world, dev)
         e2e = {"value": N * layer_steps * world / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": Lyr * N * H * 2, "d2h_bytes_per_step": Lyr * N * H * 2,
                "ms_per_step": ems / args.steps,
@@ -555,13 +561,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test mode for the multi-process code path on a one-GPU box: every rank on cuda:0 and a
+    # gloo process group (NCCL refuses two ranks on one device); only --ep --p2p and replicas
+    if os.environ.get("TIDE_BENCH_SAME_DEVICE"):
+        local_rank = 0
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
     if world > 1:
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("TIDE_BENCH_SAME_DEVICE"):
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_tide(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
