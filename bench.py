@@ -414,25 +414,31 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     # e2e: hidden states from pinned host in, output to pinned host out, every layer-step
     e2e = None
     if not args.no_e2e:
-        xh = [L["x"].cpu().pin_memory() for L in layers]
+        Ly = len(layers)
+        # inputs of step t for every layer contiguous in pinned host memory: layer 0's input
+        # goes first, layers 1.. in one copy that lands while layer 0 computes
+        xh = torch.stack([L["x"] for L in layers], 1).cpu().pin_memory()  # [T, L, N, H]
         oh = [torch.empty(N, H, dtype=torch.bfloat16).pin_memory() for _ in layers]
-        xd = [torch.empty(N, H, dtype=torch.bfloat16, device=dev) for _ in layers]
+        xd = torch.empty(Ly, N, H, dtype=torch.bfloat16, device=dev)
         cs = torch.cuda.Stream(device=dev)  # copy stream: PCIe transfers overlap the layer-steps
-        ev_in = [torch.cuda.Event() for _ in layers]
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
         ev_out = [torch.cuda.Event() for _ in layers]
 
         def e2e_step(t):
-            # every layer-step's input goes H2D on the copy stream (after the previous step's
-            # compute has consumed the buffers); each layer-step waits for its own input, and
-            # its output goes D2H on the copy stream while the next layer-step runs
+            # the step's inputs go H2D on the copy stream (after the previous step's compute has
+            # consumed the buffers); each layer-step's output goes D2H on the copy stream while
+            # the next layer-step runs
             ms = torch.cuda.current_stream()  # the capture stream under torch.cuda.graph
             cs.wait_stream(ms)
             with torch.cuda.stream(cs):
-                for li in range(len(layers)):
-                    xd[li].copy_(xh[li][t], non_blocking=True)
-                    ev_in[li].record(cs)
+                xd[0].copy_(xh[t, 0], non_blocking=True)
+                ev_in[0].record(cs)
+                if Ly > 1:
+                    xd[1:].copy_(xh[t, 1:], non_blocking=True)
+                    ev_in[1].record(cs)
             for li, L in enumerate(layers):
-                ms.wait_event(ev_in[li])
+                if li < 2:
+                    ms.wait_event(ev_in[li])
                 layer_step(L, t, x=xd[li])
                 ev_out[li].record(ms)
                 cs.wait_event(ev_out[li])
