@@ -401,6 +401,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
     flops_per_layer_step = 2 * N * k * 3 * H * F + (2 * N * 3 * H * F if s.shared_expert else 0)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
                 "traffic_detail": traffic_detail,
                 "kernel": "tide_ffn_kernel (grouped SwiGLU, tcgen05 + TMA)",
                 "peak_source": peak_src,
