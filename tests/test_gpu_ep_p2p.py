@@ -265,3 +265,50 @@ def test_p2p_emulated_world2_mini_shape_bitwise():
             assert torch.equal(hits[r], one.hit_counts), (t, r)
     for c in ctxs:
         assert c.error() == 0
+
+
+def test_p2p_emulated_world2_toy_fp32():
+    """BJ.configs[0] shapes (fp32, tf32 MMA, CUDA-core router): two emulated ranks, the peer
+    path's fp32 instances; bitwise equal to the single-device step, hits exact."""
+    from paper_2605_20179_b200 import tide
+    s = g.TOY
+    world, N, E = 2, s.tokens, s.num_experts
+    El = E // world
+    layer = DeviceLayer(s, 95)
+    desc = desc_for(s)
+    warm = tide.EPPeerContext(desc, 0, 1)
+    warm.connect(bases=[warm.export()[1]])
+    warm.moe_step_ep(g.np_to_torch(g.block_hidden_np(s, 95, steps=1)[0], "cuda"), layer.router,
+                     layer.device_all, placement=torch.zeros(E, dtype=torch.uint8, device="cuda"),
+                     step=0, interval=1)
+    torch.cuda.synchronize()
+    warm.close()
+    ctxs = [tide.EPPeerContext(desc, r, world) for r in range(world)]
+    bases = [c.export()[1] for c in ctxs]
+    for c in ctxs:
+        c.connect(bases=bases)
+    single = tide.Context(desc_for(s, max_tokens=world * N), E)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    local = [layer.device_all[r * El:(r + 1) * El].contiguous() for r in range(world)]
+    xs = [g.block_hidden_np(s, 700 + r, steps=4) for r in range(world)]
+    pl = [torch.zeros(El, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    p1 = torch.zeros(E, dtype=torch.uint8, device="cuda")
+    outs = [torch.empty(N, s.hidden, dtype=torch.float32, device="cuda") for _ in range(world)]
+    hits = [torch.empty(E, dtype=torch.int32, device="cuda") for _ in range(world)]
+    for t in range(4):
+        xin = [g.np_to_torch(xs[r][t], "cuda") for r in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                ctxs[r].moe_step_ep(xin[r], layer.router, local[r], placement=pl[r], step=t,
+                                    interval=s.interval, capacity=s.capacity // world,
+                                    out=outs[r], hit_counts=hits[r], placement_out=pl[r])
+        torch.cuda.synchronize()
+        one = single.moe_step(torch.cat(xin), layer.router, **layer.weights(), placement=p1,
+                              step=t, interval=s.interval, placement_out=p1)
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert torch.equal(outs[r].view(torch.int32), one.out[r * N:(r + 1) * N].view(torch.int32)), (t, r)
+            assert torch.equal(hits[r], one.hit_counts), (t, r)
+    for c in ctxs:
+        assert c.error() == 0
