@@ -500,8 +500,6 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     return fail(TIDE_EUNSUPPORTED, "num_experts %d not divisible by world %d", d->num_experts, world);
   if (p2p && world > kEpMaxWorld)
     return fail(TIDE_EUNSUPPORTED, "peer-memory EP supports world <= %d", kEpMaxWorld);
-  if (d->num_experts / world < d->top_k && world > 1 && false)
-    return fail(TIDE_EUNSUPPORTED, "fewer local experts than top_k");
   const int El = d->num_experts / world;
   const int max_ent = El + world * d->max_tokens * d->top_k / kMaxTok + 2 +
                       (d->max_tokens + kMaxTok - 1) / kMaxTok;
