@@ -229,13 +229,17 @@ TIDE_API tide_status tide_moe_step_ep(tide_ctx* ctx, const void* block_hidden, i
 
 /* ------------------------------------------------------------------------
  * Peer-memory expert parallelism (NEXT-3 "fused NVLink dispatch/combine", SURVEY 8(f);
- * the exchange of SURVEY 8(e) without NCCL on the data path).  Same step, same
- * arguments, same results (bitwise equal to the NCCL path for a fixed world): the
- * dispatch is a kernel that stores each token row, its top-k ids and gates straight
- * into every rank's symmetric region (P2P stores over NVLink / NVSwitch), and the
- * per-source partial sums are stored by the partial kernel straight into the source
- * rank's receive buffer; each CTA then arrives on a counter in the destination
- * (release, system scope) that the consuming kernel waits on (acquire).
+ * the exchange of SURVEY 8(e) without NCCL on the data path).  Same step and arguments
+ * as tide_moe_step_ep; the exchanges are done by the compute kernels themselves with
+ * P2P stores into every rank's symmetric region (NVLink / NVSwitch):
+ *  - dispatch fused into the router: each token row of X, its top-k ids, gates and the
+ *    rank's token count go to every rank; one release arrival per source rank;
+ *  - combine exchange fused into the grouped FFN: the tcgen05 epilogue stores each
+ *    routed pair's y row into its token's rank; the FFN's last CTA delivers the local
+ *    experts' hit counts and arrives once per rank (release, system scope);
+ *  - the token's rank then runs the single-device combine (slot order, fp32, + shared
+ *    expert), so out equals tide_moe_step's out bit for bit for every world size.
+ * Consumers wait on the arrival counters with acquire loads (system scope).
  *
  * Setup, on every rank, per layer context:
  *   tide_ctx_create_ep_p2p(desc, device, rank, world, &ctx)    (world <= 8)
