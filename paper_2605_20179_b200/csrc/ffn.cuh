@@ -478,8 +478,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
       if (item.kind == 0) {  // publish this F-tile of h to phase-2 consumers on any SM
-        __threadfence();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 128);  // the 128 epilogue threads' h stores, then one release
         if (warp == 2 && lane == 0) red_release_gpu_add(p.done + item.entry, 1);
       }
     }

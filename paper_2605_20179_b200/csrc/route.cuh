@@ -250,16 +250,15 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
                                            unsigned long long* tr, int& s_flag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int E = p.E;
-  __threadfence();
   __syncthreads();
   if (tid == 0) {
     if (tr) tr[1] = globaltimer_ns();
-    __threadfence();  // (EP: the grid's last CTA publishes everything at system scope)
-    s_flag = atomicAdd(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
+    // release this CTA's logits (and EP peer stores: the grid's last CTA publishes them at
+    // system scope); acquire the earlier arrivals' for the group's phase 2
+    s_flag = atom_add_acq_rel_gpu(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
   if (!s_flag) return;
-  __threadfence();
   if (tid == 0) {
     p.g_cnt[blockIdx.y] = 0;
     if (tr) tr[2] = globaltimer_ns();
@@ -290,11 +289,9 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
-    __threadfence();
-    if (atomicAdd(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
+    if (atom_add_acq_rel_gpu(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
-      __threadfence();
       if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
                      // g_cnt / g_done chains; one system-scope fence publishes them: arrive
         for (int dst = 0; dst < p.ep_P; ++dst)
