@@ -98,8 +98,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   constexpr int KSTEPS = BK / UK;
 
   extern __shared__ uint8_t ffn_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(ffn_smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SW128 tiles); offsetting the shared array itself keeps the shared
+  // state space visible to the compiler (LDS/STS, not generic loads/stores)
+  uint8_t* smem = ffn_smem_raw + ((1024u - (smem_u32(ffn_smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
