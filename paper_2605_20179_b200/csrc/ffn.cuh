@@ -139,11 +139,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_trigger();  // the combine grid may start its prologue
+  // routing (counts, token lists, x_in) comes from the preceding grid; the dependent grid
+  // (combine) may launch once every CTA is past that wait, so it can read the routing it
+  // needs (top-k, slots, gates) before its own wait on this grid
+  if (warp == 0) pdl_wait();
+  __syncthreads();
+  pdl_trigger();
 
   if (warp == 0) {
     // ===================== scheduler + TMA producer =====================
-    pdl_wait();  // routing (counts, token lists, x_in) comes from the preceding grid
     if (tr && lane == 0) tr[5] = globaltimer_ns();
     int n_ent;
     const int4* ents = p.entries;

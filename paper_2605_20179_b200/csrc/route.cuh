@@ -630,20 +630,23 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            T* __restrict__ out, int N, int k,
                                                            int H, int shared,
                                                            unsigned long long* trace) {
-  pdl_wait();
-  pdl_trigger();
-  if (trace && threadIdx.x == 0) atomicMax(trace, globaltimer_ns());  // debug: latest start
   const int n = blockIdx.x, lane = threadIdx.x & 31;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  // lane j < k fetches pair j's row and gate (one round of independent loads), then the
-  // y rows are read with all loads of an unrolled group in flight
-  int r_j = 0;
+  // lane j < k fetches pair j's expert, slot and gate before the wait: the route kernel that
+  // wrote them completed before the FFN (the preceding grid) triggered this launch; off[]
+  // and y come from the FFN itself, after the wait
+  int e_j = 0, s_j = 0, r_j = 0;
   float g_j = 0.f;
   if (lane < k) {
     const int q = n * k + lane;
-    r_j = __ldcg(off + __ldcg(topk + q)) + __ldcg(pair_slot + q);
+    e_j = __ldcg(topk + q);
+    s_j = __ldcg(pair_slot + q);
     g_j = __ldcg(gates + q);
   }
+  pdl_wait();
+  pdl_trigger();
+  if (trace && threadIdx.x == 0) atomicMax(trace, globaltimer_ns());  // debug: latest start
+  if (lane < k) r_j = __ldcg(off + e_j) + s_j;
   const bool valid = c < H;  // (lanes stay converged for the shuffles)
   const int cc = valid ? c : 0;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
