@@ -467,11 +467,14 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) s_red[warp][lane][r] = acc[r];
-    // x_in copy (the FFN's gather source) by the first expert tile of each token group
-    if (blockIdx.x == 0) {
+    // x_in copy (the FFN's gather source), spread over the token group's expert tiles: CTA bx
+    // copies uint4 columns [bx*per, (bx+1)*per) of the group's rows (no straggler CTA)
+    {
       const int per_row = H / 8;  // uint4 per row
-      for (int i = tid; i < (n1 - n0) * per_row; i += blockDim.x) {
-        const int n = n0 + i / per_row, q = i % per_row;
+      const int per = (per_row + (int)gridDim.x - 1) / (int)gridDim.x;
+      const int q0 = blockIdx.x * per, w = min(per_row, q0 + per) - q0;
+      for (int i = tid; i < (n1 - n0) * w; i += blockDim.x) {
+        const int n = n0 + i / w, q = q0 + i % w;
         reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.x_in) + (size_t)n * H)[q] =
             __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) + (size_t)n * H) + q);
       }
