@@ -880,8 +880,11 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
     rp.tpc = 8;
     const dim3 grid(E / 16, std::max(1, (N + 7) / 8));
     cudaError_t le;
-#define TC_LAUNCH(EP) \
-  le = launch_pdl(tide_route_tc_kernel<EP, 8, 1>, grid, dim3(kRouteThreads), 0, st, rp)
+    // large batches (more than one wave of 16 x 8 tiles): two CTAs per SM (<= 128 registers)
+    const bool two_per_sm = grid.x * grid.y > (unsigned)c->num_sms && !getenv("TIDE_ROUTE_ONE_PER_SM");
+#define TC_LAUNCH(EP)                                                                        \
+  le = two_per_sm ? launch_pdl(tide_route_tc_kernel<EP, 8, 2>, grid, dim3(kRouteThreads), 0, st, rp) \
+                  : launch_pdl(tide_route_tc_kernel<EP, 8, 1>, grid, dim3(kRouteThreads), 0, st, rp)
     switch (route_epl(E)) {
       case 1: TC_LAUNCH(1); break;
       case 2: TC_LAUNCH(2); break;
