@@ -145,89 +145,101 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   if (warp == 0) pdl_wait();
   __syncthreads();
   pdl_trigger();
+  if (tr && threadIdx.x == 0) tr[5] = globaltimer_ns();
 
-  if (warp == 0) {
-    // ===================== scheduler + TMA producer =====================
-    if (tr && lane == 0) tr[5] = globaltimer_ns();
-    int n_ent;
-    const int4* ents = p.entries;
-    if (p.cnt) {  // build this CTA's copy of the work list (warp 0, expert ranges per lane)
-      const int E = p.E;
-      const int per = (E + 31) >> 5, e0 = min(E, lane * per), e1 = min(E, e0 + per);
-      int rows = 0, nent = 0, rows_x, ent_x;
-      if (per <= 8) {
-        // E <= 256: one batch of independent loads per lane (both count halves, the parity
-        // word and the slots), selected in registers: one L2 round trip, not a dependent chain
-        int m8[8], s8[8], mb[8];
-        const int pr = p.par ? __ldcg(p.par) : 1;
+  // Work list (build mode): every thread of the CTA takes a contiguous range of experts, loads
+  // their counts in one batch (both count halves, the parity word and the slots: one L2 round
+  // trip, no dependent chain), then a CTA-wide exclusive scan of (rows, entries) places each
+  // expert's entries in s_ent and (CTA 0) its first FFN row in off_out.
+  __shared__ int s_wsum[2][kFfnThreads / 32];
+  __shared__ int s_nent;
+  if (p.cnt) {
+    const int E = p.E, t = threadIdx.x;
+    constexpr int PER = 4;  // experts per thread in the batched path (E <= 4 * 192)
+    const int per = (E + kFfnThreads - 1) / kFfnThreads;
+    int rows = 0, nent = 0;
+    int m4[PER], s4[PER];
+    const int e0 = min(E, t * per), e1 = min(E, e0 + per);
+    if (per <= PER) {
+      int mb[PER];
+      const int pr = p.par ? __ldcg(p.par) : 1;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i;
-          const bool ok = e < e1;
-          m8[i] = ok ? __ldcg(p.cnt + e) : 0;
-          mb[i] = (ok && p.par) ? __ldcg(p.cnt + E + e) : 0;
-          s8[i] = ok ? (p.slot_of ? __ldcg(p.slot_of + e) : e) : -1;
-        }
+      for (int i = 0; i < PER; ++i) {
+        const int e = e0 + i;
+        const bool ok = e < e1;
+        m4[i] = ok ? __ldcg(p.cnt + e) : 0;
+        mb[i] = (ok && p.par) ? __ldcg(p.cnt + E + e) : 0;
+        s4[i] = ok ? (p.slot_of ? __ldcg(p.slot_of + e) : e) : -1;
+      }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (pr == 0) m8[i] = mb[i];  // this step's counts live in cnt[par ^ 1]
-          rows += m8[i];
-          nent += (m8[i] > 0 && s8[i] >= 0) ? (m8[i] + kMaxTok - 1) / kMaxTok : 0;
-        }
-        rows_x = rows; ent_x = nent;  // inclusive warp scans -> exclusive bases
+      for (int i = 0; i < PER; ++i) {
+        if (pr == 0) m4[i] = mb[i];  // this step's counts live in cnt[par ^ 1]
+        rows += m4[i];
+        nent += (m4[i] > 0 && s4[i] >= 0) ? (m4[i] + kMaxTok - 1) / kMaxTok : 0;
+      }
+    } else {  // very large E: per-expert loop (not on the benchmarked shapes)
+      const int* cnt = p.par ? p.cnt + (__ldcg(p.par) ^ 1) * E : p.cnt;
+      for (int e = e0; e < e1; ++e) {
+        const int m = __ldcg(cnt + e);
+        const bool in_hbm = !p.slot_of || __ldcg(p.slot_of + e) >= 0;
+        rows += m;
+        nent += (m > 0 && in_hbm) ? (m + kMaxTok - 1) / kMaxTok : 0;
+      }
+    }
+    int rows_x = rows, ent_x = nent;  // warp inclusive scans, then the warps' prefixes
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int a = __shfl_up_sync(0xffffffffu, rows_x, o), b = __shfl_up_sync(0xffffffffu, ent_x, o);
-          if (lane >= o) { rows_x += a; ent_x += b; }
-        }
-        int row = rows_x - rows, ei = ent_x - nent;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, rows_x, o), b = __shfl_up_sync(0xffffffffu, ent_x, o);
+      if (lane >= o) { rows_x += a; ent_x += b; }
+    }
+    if (lane == 31) { s_wsum[0][warp] = rows_x; s_wsum[1][warp] = ent_x; }
+    __syncthreads();
+    int row = rows_x - rows, ei = ent_x - nent;
+    for (int w = 0; w < warp; ++w) { row += s_wsum[0][w]; ei += s_wsum[1][w]; }
+    if (per <= PER) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i, m = m8[i];
-          if (e < e1) {
-            if (blockIdx.x == 0) p.off_out[e] = row;
-            if (m > 0 && s8[i] >= 0)
-              for (int c = 0; c * kMaxTok < m; ++c)
-                s_ent[ei++] = make_int4(s8[i], row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
-                                        e * p.maxN + c * kMaxTok);
-            row += m;
-          }
-        }
-      } else {
-        const int* cnt = p.par ? p.cnt + (__ldcg(p.par) ^ 1) * E : p.cnt;
-        for (int e = e0; e < e1; ++e) {
-          const int m = __ldcg(cnt + e);
-          const bool in_hbm = !p.slot_of || __ldcg(p.slot_of + e) >= 0;
-          rows += m;
-          nent += (m > 0 && in_hbm) ? (m + kMaxTok - 1) / kMaxTok : 0;
-        }
-        rows_x = rows; ent_x = nent;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int a = __shfl_up_sync(0xffffffffu, rows_x, o), b = __shfl_up_sync(0xffffffffu, ent_x, o);
-          if (lane >= o) { rows_x += a; ent_x += b; }
-        }
-        int row = rows_x - rows, ei = ent_x - nent;
-        for (int e = e0; e < e1; ++e) {
-          const int m = __ldcg(cnt + e);
-          const int slot = p.slot_of ? __ldcg(p.slot_of + e) : e;
+      for (int i = 0; i < PER; ++i) {
+        const int e = e0 + i, m = m4[i];
+        if (e < e1) {
           if (blockIdx.x == 0) p.off_out[e] = row;
-          if (m > 0 && slot >= 0)
+          if (m > 0 && s4[i] >= 0)
             for (int c = 0; c * kMaxTok < m; ++c)
-              s_ent[ei++] = make_int4(slot, row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
+              s_ent[ei++] = make_int4(s4[i], row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
                                       e * p.maxN + c * kMaxTok);
           row += m;
         }
       }
-      n_ent = __shfl_sync(0xffffffffu, ent_x, 31);
-      const int n_sh = p.shared ? (p.N + kMaxTok - 1) / kMaxTok : 0;
-      for (int c = lane; c < n_sh; c += 32)
-        s_ent[n_ent + c] = make_int4(0, p.shared_row0 + c * kMaxTok,
-                                     min(kMaxTok, p.N - c * kMaxTok) | (3 << 16),
-                                     p.shared_tok0 + c * kMaxTok);
-      n_ent += n_sh;
+    } else {
+      const int* cnt = p.par ? p.cnt + (__ldcg(p.par) ^ 1) * E : p.cnt;
+      for (int e = e0; e < e1; ++e) {
+        const int m = __ldcg(cnt + e);
+        const int slot = p.slot_of ? __ldcg(p.slot_of + e) : e;
+        if (blockIdx.x == 0) p.off_out[e] = row;
+        if (m > 0 && slot >= 0)
+          for (int c = 0; c * kMaxTok < m; ++c)
+            s_ent[ei++] = make_int4(slot, row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
+                                    e * p.maxN + c * kMaxTok);
+        row += m;
+      }
+    }
+    int n_r = 0;  // routed entries in total
+    for (int w = 0; w < kFfnThreads / 32; ++w) n_r += s_wsum[1][w];
+    const int n_sh = p.shared ? (p.N + kMaxTok - 1) / kMaxTok : 0;
+    for (int c = t; c < n_sh; c += kFfnThreads)
+      s_ent[n_r + c] = make_int4(0, p.shared_row0 + c * kMaxTok,
+                                 min(kMaxTok, p.N - c * kMaxTok) | (3 << 16),
+                                 p.shared_tok0 + c * kMaxTok);
+    if (t == 0) s_nent = n_r + n_sh;
+    __syncthreads();
+  }
+
+  if (warp == 0) {
+    // ===================== scheduler + TMA producer =====================
+    int n_ent;
+    const int4* ents = p.entries;
+    if (p.cnt) {
+      n_ent = s_nent;
       ents = s_ent;
-      __syncwarp();
     } else {
       n_ent = *p.n_entries;
     }
