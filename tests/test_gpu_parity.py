@@ -273,3 +273,14 @@ def test_router_logit_error(shape_name, tokens):
     torch.cuda.synchronize()
     err = np.abs(r.debug["logits"].cpu().numpy().astype(np.float64) - ref).max()
     assert err < 6e-7, f"max |logit - fp64| = {err:.3e}"
+
+
+@pytest.mark.parametrize("E,H", [(1024, 128), (800, 256), (768, 256)])
+def test_many_experts_work_list_paths(E, H):
+    """E up to the descriptor limit: the FFN work list takes its batched path (E <= 768,
+    at most 4 experts per thread) or its per-expert loop (E > 768); both against the oracle."""
+    shape = g.Shape("wide", E, 4, H, 128, 1, 40, steps=1, dtype="bf16", shared_expert=True)
+    layer = DeviceLayer(shape, 19)
+    ctx = _ctx(shape, E)
+    x = g.block_hidden_np(shape, 19, steps=1)[0]
+    _run_and_check(shape, 19, x, layer, ctx, np.zeros(E, np.uint8), 0, 1, E)
