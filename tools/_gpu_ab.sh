@@ -1,4 +1,4 @@
-# A/B on one box: ab_old/ = a committed reference checkout, . = working tree
+# A/B on one box: ab_old/ = a reference checkout (git worktree add ab_old <ref>; copy MEASURED_PEAKS.json in), . = working tree
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build rc=$?
 (cd ab_old && python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1; echo old build rc=$?)
 for rep in 1 2 3; do
