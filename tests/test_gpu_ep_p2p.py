@@ -312,3 +312,48 @@ def test_p2p_emulated_world2_toy_fp32():
             assert torch.equal(hits[r], one.hit_counts), (t, r)
     for c in ctxs:
         assert c.error() == 0
+
+
+def test_p2p_world1_graph_replay_bitwise():
+    """The peer-memory EP step holds no host state per call (parity-double-buffered counters):
+    per-step CUDA graphs of it replay bitwise equal to the single-device step, over two blocks."""
+    from paper_2605_20179_b200 import tide
+    layer = DeviceLayer(SHAPE, 97)
+    desc = desc_for(SHAPE)
+    E, N, T = SHAPE.num_experts, SHAPE.tokens, SHAPE.steps
+    ctx = tide.EPPeerContext(desc, 0, 1)
+    ctx.connect(bases=[ctx.export()[1]])
+    single = tide.Context(desc, E)
+    xs = torch.stack([g.np_to_torch(x, "cuda") for x in g.block_hidden_np(SHAPE, 97)])
+    pl, p1 = (torch.zeros(E, dtype=torch.uint8, device="cuda") for _ in range(2))
+    out = torch.empty(N, SHAPE.hidden, dtype=torch.bfloat16, device="cuda")
+    hits = torch.empty(E, dtype=torch.int32, device="cuda")
+
+    def step(t):
+        ctx.moe_step_ep(xs[t], layer.router, layer.device_all, shared_w=layer.shared,
+                        placement=pl, step=t, interval=2, out=out, hit_counts=hits,
+                        placement_out=pl)
+
+    s = torch.cuda.Stream()  # warm-up off the capture stream, as torch requires
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(0)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graphs = []
+    for t in range(T):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            step(t)
+        graphs.append(gr)
+    torch.cuda.synchronize()
+    pl.zero_()
+    for blk in range(2):
+        for t in range(T):
+            graphs[t].replay()
+            ref = single.moe_step(xs[t], layer.router, **layer.weights(), placement=p1, step=t,
+                                  interval=2, placement_out=p1)
+            torch.cuda.synchronize()
+            assert torch.equal(out.view(torch.int16), ref.out.view(torch.int16)), (blk, t)
+            assert torch.equal(hits, ref.hit_counts) and torch.equal(pl, p1), (blk, t)
+    assert ctx.error() == 0
