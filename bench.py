@@ -58,7 +58,7 @@ def parse():
                          "case (alpha=0, a0=0, skew=0: the most unique experts per launch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--eager", action="store_true",
                     help="launch every layer-step from the host in the timed region (default: "
                          "NEXT-3 CUDA graphs, one per block step t covering all layers)")
@@ -137,17 +137,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ oracle baseline
-def oracle_rate(shape: g.Shape, seed: int, budget_s: float, tokens: int, wt_host=None):
-    """Time the fp64 CPU oracle (as it stands, single thread) on full layer-steps
+def oracle_rate(shape: g.Shape, seed: int, budget_s: float, tokens: int, threads: int,
+                wt_host=None, routing: str = "calibrated"):
+    """Time the fp64 CPU oracle (as it stands) on `threads` host threads, on full layer-steps
     of `tokens` tokens of layer 0, until `budget_s` seconds are spent."""
     import oracle
+    uni = routing == "uniform"
     if wt_host is None:
-        wr, wg, wu, wd, sh = g.layer_torch(shape, seed, 0, "cpu")
+        wr, wg, wu, wd, sh = g.layer_torch(shape, seed, 0, "cpu", skew=0.0 if uni else g.SKEW)
         to = g.torch_to_np
         wt_host = oracle.Layer(to(wr), to(wg), to(wu), to(wd),
                                tuple(to(a) for a in sh) if sh else None)
-    xs = g.block_hidden_np(shape, seed, 0, steps=shape.steps, tokens=tokens)
+    xs = g.block_hidden_np(shape, seed, 0, steps=shape.steps, tokens=tokens, iid=uni)
     E = shape.num_experts
+    oracle.set_threads(threads)
+    used = oracle.get_threads()
     p = np.zeros(E, np.uint8)
     n_steps, t0 = 0, time.perf_counter()
     times = []
@@ -161,10 +165,32 @@ def oracle_rate(shape: g.Shape, seed: int, budget_s: float, tokens: int, wt_host
         if time.perf_counter() - t0 > budget_s:
             break
     el = sum(times)
-    return {"value": tokens * n_steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n_steps} full layer-steps (router..combine, fp64, single thread) of "
-                      f"layer 0, {tokens} tokens each, steps 0..{n_steps - 1} of the block",
-            "ms_per_layer_step": 1e3 * el / n_steps}, times
+    return {"value": round(tokens * n_steps / el, 3), "unit": UNIT, "cores": used,
+            "kind": "oracle",
+            "sample": f"{n_steps} full layer-steps (router..combine, fp64, {used} host thread(s), "
+                      f"OpenMP over tokens) of layer 0, {tokens} tokens each, steps "
+                      f"0..{n_steps - 1} of the block",
+            "ms_per_layer_step": round(1e3 * el / n_steps, 3)}, wt_host
+
+
+def cpu_baseline(shape: g.Shape, seed: int, budget_s: float, tokens: int, routing: str):
+    """The oracle on every host core (the figure of record) and on one core, same sample."""
+    ncores = os.cpu_count() or 1
+    many, wt = oracle_rate(shape, seed, budget_s * 0.5, tokens, ncores, routing=routing)
+    one, _ = oracle_rate(shape, seed, budget_s * 0.5, tokens, 1, wt_host=wt, routing=routing)
+    many["single_thread"] = {k: one[k] for k in ("value", "cores", "sample", "ms_per_layer_step")}
+    many["host_cpu"] = _cpu_model()
+    return many
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs"
 
 
 # ------------------------------------------------------------------ main arm
@@ -483,7 +509,7 @@ def run_tide(args, rank: int, world: int, local_rank: int):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
-        cpu, _ = oracle_rate(s, args.seed, args.cpu_seconds, tokens=min(N, 32))
+        cpu = cpu_baseline(s, args.seed, args.cpu_seconds, min(N, 32), args.routing)
 
     io = None
     if pool_mode:  # a6: the H2D link is the roofline of capacity-limited steps
@@ -525,11 +551,12 @@ def run_tide(args, rank: int, world: int, local_rank: int):
 
 
 def run_reference(args):
-    """Reference arm of this tier: the fp64 CPU oracle, as it stands, timed on the
-    host cores on a bounded sample of the bench workload."""
+    """Reference arm of this tier: the fp64 CPU oracle, as it stands, timed on every host core
+    (OpenMP over tokens) on the bench workload's layer-steps (layer 0 of the stack, the
+    block's full token count)."""
     import oracle
     s = shape_for(args)
-    N = min(s.tokens, 8)
+    N = s.tokens
     uni = args.routing == "uniform"
     wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, 0, "cpu", skew=0.0 if uni else g.SKEW)
     to = g.torch_to_np
@@ -537,6 +564,8 @@ def run_reference(args):
     xs = g.block_hidden_np(s, args.seed, 0, steps=s.steps, tokens=N, iid=uni)
     E = s.num_experts
     cap = args.capacity or E
+    oracle.set_threads(os.cpu_count() or 1)
+    cores = oracle.get_threads()
     p = np.zeros(E, np.uint8)
     for i in range(args.warmup):
         p = oracle.moe_step(L, xs[i % s.steps], s.top_k, p, i % s.steps, args.interval, cap).placement
@@ -546,8 +575,8 @@ def run_reference(args):
         p = oracle.moe_step(L, xs[t], s.top_k, p, t, args.interval, cap).placement
     el = time.perf_counter() - t0
     v = N * args.steps / el
-    sample = (f"each step = one full layer-step (router..combine, fp64, single thread) of layer 0 "
-              f"on {N} of the block's {s.tokens} tokens")
+    sample = (f"each step = one full layer-step (router..combine, fp64, {cores} host threads, "
+              f"OpenMP over tokens) of layer 0 of the stack on all {N} tokens of the block")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * el / args.steps, 2), "higher_is_better": True,
@@ -556,9 +585,9 @@ def run_reference(args):
                        "tokens_per_layer_step": s.tokens, "num_experts": E, "top_k": s.top_k,
                        "hidden": s.hidden, "ffn": s.ffn, "capacity": cap,
                        "interval": args.interval, "routing": args.routing,
-                       "oracle_sample": f"{N} of {s.tokens} tokens of layer 0 per step"},
-            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                       "oracle_sample": f"layer 0 of {s.layers}, all {N} tokens per step"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample, "host_cpu": _cpu_model()},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 

@@ -27,7 +27,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain C99, fp64, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(
-            ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+            ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
              "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
@@ -41,6 +41,15 @@ def lib():
         build()
         _lib = ctypes.CDLL(_LIB)
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Host threads for the oracle's per-token loops (bit-identical results for any n)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
 
 
 def _p(a):

@@ -17,6 +17,28 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threading (bench.py's cpu_baseline runs the oracle on 1 and on nproc host cores).  Only
+ * loops over independent tokens are split across threads; every token's arithmetic runs in
+ * the same order on one thread, so results are bit-identical for any thread count
+ * (pinned by tests/test_oracle_pins.py::test_threads_bit_identical). */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+#else
+  (void)n;
+#endif
+}
+int orc_get_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
 
 /* Exact conversion of a stored element to double.  bf16 is the top half of
  * an IEEE binary32, so widening is exact.                                 */
@@ -36,6 +58,7 @@ static double rd(const void* base, int dtype, size_t i) {
 int orc_router_logits(int N, int E, int hidden, const void* x, int x_dtype, const void* wr,
                       int wr_dtype, double* logits) {
   if (N < 0 || E <= 0 || hidden <= 0) return 1;
+#pragma omp parallel for schedule(static)
   for (int n = 0; n < N; ++n)
     for (int e = 0; e < E; ++e) {
       double s = 0.0;
@@ -195,26 +218,43 @@ int orc_combine(const orc_layer* L, int N, const void* x, const int32_t* topk_id
                 const void* const* wd, const void* swg, const void* swu, const void* swd,
                 const uint8_t* token_mask, double* out) {
   const int H = L->hidden, F = L->ffn, k = L->top_k;
-  double* xn = (double*)malloc(sizeof(double) * (size_t)H);
-  double* y = (double*)malloc(sizeof(double) * (size_t)H);
+  const int per = k + (L->shared_expert ? 1 : 0); /* expert evaluations per token */
+  /* y of every (token, slot) pair -- independent SwiGLUs, evaluated on any host thread --
+   * then each token's sum in slot order, exactly as written in P:303. */
+  double* ys = (double*)malloc(sizeof(double) * (size_t)N * per * H);
+#pragma omp parallel
+  {
+    double* xn = (double*)malloc(sizeof(double) * (size_t)H);
+#pragma omp for schedule(dynamic, 1)
+    for (int q = 0; q < N * per; ++q) {
+      const int n = q / per, j = q % per;
+      if (token_mask && !token_mask[n]) continue;
+      for (int h = 0; h < H; ++h) xn[h] = rd(x, L->act_dtype, (size_t)n * H + h);
+      double* y = ys + (size_t)q * H;
+      if (j < k) {
+        const int e = topk_idx[(size_t)n * k + j];
+        orc_swiglu(H, F, xn, wg[e], wu[e], wd[e], L->weight_dtype, y);
+      } else { /* R-16: the shared expert */
+        orc_swiglu(H, F, xn, swg, swu, swd, L->weight_dtype, y);
+      }
+    }
+    free(xn);
+  }
   for (int n = 0; n < N; ++n) {
     double* o = out + (size_t)n * H;
     for (int h = 0; h < H; ++h) o[h] = 0.0;
     if (token_mask && !token_mask[n]) continue;
-    for (int h = 0; h < H; ++h) xn[h] = rd(x, L->act_dtype, (size_t)n * H + h);
     for (int j = 0; j < k; ++j) {
-      int e = topk_idx[(size_t)n * k + j];
-      orc_swiglu(H, F, xn, wg[e], wu[e], wd[e], L->weight_dtype, y);
-      double g = gates[(size_t)n * k + j];
+      const double g = gates[(size_t)n * k + j];
+      const double* y = ys + ((size_t)n * per + j) * H;
       for (int h = 0; h < H; ++h) o[h] += g * y[h];
     }
     if (L->shared_expert) { /* R-16: weight 1, always resident, not counted */
-      orc_swiglu(H, F, xn, swg, swu, swd, L->weight_dtype, y);
+      const double* y = ys + ((size_t)n * per + k) * H;
       for (int h = 0; h < H; ++h) o[h] += y[h];
     }
   }
-  free(xn);
-  free(y);
+  free(ys);
   return 0;
 }
 
@@ -302,14 +342,22 @@ int orc_ep_step(const orc_layer* L, int P, int N, const void* x, const void* wr,
   for (size_t i = 0; i < (size_t)N * H; ++i) out[i] = 0.0;
   for (int r = 0; r < P; ++r) {
     for (size_t i = 0; i < (size_t)N * H; ++i) part[i] = 0.0;
-    for (int n = 0; n < N; ++n) {
-      for (int h = 0; h < H; ++h) xn[h] = rd(x, L->act_dtype, (size_t)n * H + h);
-      for (int j = 0; j < k; ++j) {
-        int e = topk_idx[(size_t)n * k + j];
-        if (e / El != r) continue;
-        orc_swiglu(H, L->ffn, xn, wg[e], wu[e], wd[e], L->weight_dtype, y);
-        for (int h = 0; h < H; ++h) part[(size_t)n * H + h] += gates[(size_t)n * k + j] * y[h];
+#pragma omp parallel
+    {
+      double* xt = (double*)malloc(sizeof(double) * (size_t)H);
+      double* yt = (double*)malloc(sizeof(double) * (size_t)H);
+#pragma omp for schedule(dynamic, 1)
+      for (int n = 0; n < N; ++n) {
+        for (int h = 0; h < H; ++h) xt[h] = rd(x, L->act_dtype, (size_t)n * H + h);
+        for (int j = 0; j < k; ++j) {
+          int e = topk_idx[(size_t)n * k + j];
+          if (e / El != r) continue;
+          orc_swiglu(H, L->ffn, xt, wg[e], wu[e], wd[e], L->weight_dtype, yt);
+          for (int h = 0; h < H; ++h) part[(size_t)n * H + h] += gates[(size_t)n * k + j] * yt[h];
+        }
       }
+      free(xt);
+      free(yt);
     }
     for (size_t i = 0; i < (size_t)N * H; ++i) out[i] += part[i];
   }

@@ -23,6 +23,11 @@ extern "C" {
 
 enum { ORC_F32 = 0, ORC_BF16 = 1 };
 
+/* Host threads for the per-token loops (OpenMP).  Results are bit-identical for any
+ * count: a token's arithmetic never crosses threads.                                */
+void orc_set_threads(int n);
+int orc_get_threads(void);
+
 /* O1: logits[n*E+e] = sum_h x[n,h]*wr[e,h], summed in h order. */
 int orc_router_logits(int N, int E, int hidden, const void* x, int x_dtype,
                       const void* wr, int wr_dtype, double* logits);

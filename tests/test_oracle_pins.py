@@ -424,3 +424,45 @@ def test_ep_emulation_equals_single_device(P):
     for r in range(P):
         want = {r * El + e for e in _brute_top_c(h[r * El:(r + 1) * El], cr)}
         assert set(np.nonzero(pout[r * El:(r + 1) * El])[0] + r * El) == want
+
+
+# ------------------------------------------------------------------ O10 eviction timing (R-12)
+def test_io_eviction_timing_hand_worked():
+    """O10 vs a hand-worked three-step example (tests/golden/io_eviction_timing.json, DESIGN
+    R-12/R-13): an expert evicted at a refresh is still served from HBM in that step, so it is
+    not streamed; the alternative rule (evict before counting) would stream it."""
+    ex = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                     "io_eviction_timing.json")))
+    E = ex["E"]
+    loaded = np.zeros(E, np.uint8)
+    for st in ex["steps"]:
+        h = np.array(st["hits"], np.int32)
+        pin = np.array(st["placement_in"], np.uint8)
+        po = oracle.placement(h, ex["capacity"], st["refresh"], pin)
+        assert po.tolist() == st["placement_out"], st["step"]
+        io = oracle.io_step(h, pin, po, loaded, lazy=bool(ex["lazy"]))
+        assert io == st["expect"], (st["step"], io)
+        assert loaded.tolist() == st["loaded_after"], st["step"]
+
+
+# ------------------------------------------------------------------ threading
+def test_threads_bit_identical():
+    """The oracle's per-token loops run on host threads (bench.py cpu_baseline on nproc cores);
+    a token's arithmetic never crosses threads, so 1 and 4 threads give identical bits for the
+    whole step (O1..O9) and the EP emulation (O11)."""
+    shp, L = _tiny_layer(77, E=8, H=64, F=64, shared=True)
+    x = g.block_hidden_np(shp, 77, tokens=23)[0]
+    E, k = shp.num_experts, shp.top_k
+    res = []
+    for nt in (1, 4):
+        oracle.set_threads(nt)
+        assert oracle.get_threads() == nt
+        r = oracle.moe_step(L, x, k, np.zeros(E, np.uint8), 0, 1, 3)
+        ep = oracle.ep_step(L, 2, x, k, np.zeros(E, np.uint8), 0, 1, 2)
+        res.append((r, ep))
+    oracle.set_threads(os.cpu_count() or 1)
+    (a, ea), (b, eb) = res
+    assert a.logits.tobytes() == b.logits.tobytes()
+    assert a.out.tobytes() == b.out.tobytes()
+    assert (a.topk_idx == b.topk_idx).all() and (a.pos == b.pos).all()
+    assert ea[3].tobytes() == eb[3].tobytes()
