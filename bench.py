@@ -1,29 +1,39 @@
 #!/usr/bin/env python
 """bench.py -- block-tokens/s per MoE layer-step of the TIDE hot path on B200.
 
-One bench *step* = one denoising step of the block through every MoE layer of
-the stack (20 layers for the mini config); each layer-step is the whole hot
-path (router, top-k, hits, refresh/placement, permutation, grouped SwiGLU FFN
-on tcgen05, combine; pinned-host serving when capacity < E), one
-tide_moe_step call through the C ABI.
+One bench *step* = one denoising step of the block(s) through every MoE layer of the
+stack; each layer-step is the whole hot path (router, top-k, hits, refresh/placement,
+permutation, grouped SwiGLU FFN on tcgen05, combine; pinned-host serving when
+capacity < E; the expert-parallel exchange under EP), one tide_moe_step /
+tide_moe_step_ep call through the C ABI.
 
-  value  = tokens x layer-steps / device time (CUDA events, max over ranks)
-  e2e    = same metric with the block's hidden states H2D-copied from pinned
-           host before, and the output D2H-copied after, every layer-step
-  roofline = the grouped FFN kernel's algorithmic HBM bytes / its measured
-           average launch time vs MEASURED_PEAKS.json hbm_gbs
+  value    = tokens x layer-steps, summed over ranks / device time (CUDA events, max over
+             ranks)
+  e2e      = same metric with every layer-step's hidden states H2D-copied from pinned host
+             and its output D2H-copied, inside the timed region
+  roofline = the dominant kernel's algorithmic bytes / its measured launch time vs
+             MEASURED_PEAKS.json (the grouped FFN and HBM when every expert is in HBM; the
+             H2D link when capacity < E)
 
-`--impl reference` times the fp64 CPU oracle (the reference arm of this tier)
-on a bounded sample of the same workload.  Multi-GPU (torchrun): every rank
-runs its own blocks through its own replica of the stack (weak scaling, no
-data-path collective); EP is listed in DESIGN.md as next.
+N = 1 (default): BJ.configs[1] (mini stack, C = E) is the headline; `sub_results` adds the
+8-block sweep batch (BJ.configs[4], C = E) and the flash-shaped stack with pinned-host
+serving at the paper's budget C = 64 and at C = 217 (BJ.configs[2], 8 of 32 layers: the
+full stack does not fit one GPU).
+N > 1 (`--gpus N`, spawned through torchrun when WORLD_SIZE is unset): BJ.configs[3], the
+flash-shaped 32-layer stack expert-parallel over the N GPUs (E/N experts per rank, all in
+HBM), one block per rank (weak scaling), dispatch/combine inside the kernels over peer
+memory (NVLink); the NCCL all-gather / all-to-all variant is reported beside it.
+`--replicas` runs independent per-rank stacks instead.
+
+`--impl reference` times the fp64 CPU oracle (the reference arm of this tier) on every host
+core on the same workload's layer-steps.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,6 +50,15 @@ import tidegen as g  # noqa: E402
 
 METRIC = "block-tokens/sec per MoE layer-step"
 UNIT = "block-tokens/s"
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (SURVEY 8(d) metric 5)
+PAPER_CONTEXT = {
+    "note": "The paper's published numbers are end-to-end dLLM decode speed-ups of its GPU-CPU "
+            "system over baselines, on other hardware and with real LLaDA2.0 weights; they are "
+            "context, not a target for this layer-step metric (vs_baseline is null).",
+    "speedup_vs_best_baseline": "1.4x (LLaDA2.0-mini) / 1.5x (LLaDA2.0-flash) decode throughput "
+                                "(P:14, P:440)",
+    "hardware": "NVIDIA A100 80GB and H100 80GB + host CPU (48-core), PCIe (P:350)",
+}
 
 
 def parse():
@@ -48,7 +67,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["tide", "reference"], default="tide")
-    ap.add_argument("--config", choices=["mini", "sweep", "flash1"], default="mini")
+    ap.add_argument("--config", choices=["mini", "sweep", "flash1", "flash"], default=None,
+                    help="default: mini at N=1, flash (expert parallel) at N>1")
     ap.add_argument("--capacity", type=int, default=0, help="0 = all experts in HBM (C = E)")
     ap.add_argument("--interval", type=int, default=4)
     ap.add_argument("--layers", type=int, default=0, help="override the stack depth")
@@ -58,6 +78,7 @@ def parse():
                          "case (alpha=0, a0=0, skew=0: the most unique experts per launch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the sub-results")
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--eager", action="store_true",
                     help="launch every layer-step from the host in the timed region (default: "
@@ -66,33 +87,41 @@ def parse():
                     help="NEXT-3 cross-layer L2 prefetch budget per layer-step (MB); "
                          "-1 = default (32 MB when all experts are in HBM), 0 = off")
     ap.add_argument("--ep", action="store_true",
-                    help="expert parallelism over the ranks (tide_moe_step_ep) instead of replicas")
+                    help="expert parallelism over the ranks (default at N>1; also at N=1)")
     ap.add_argument("--p2p", action="store_true",
-                    help="with --ep: dispatch/combine by the kernels over peer memory "
-                         "(tide_ctx_create_ep_p2p) instead of NCCL collectives")
+                    help="with --ep at N=1: dispatch/combine by the kernels over peer memory "
+                         "(the N>1 default)")
+    ap.add_argument("--nccl", action="store_true",
+                    help="EP headline on the NCCL collectives instead of peer memory")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent per-rank stacks (no data-path collective) instead of EP")
     return ap.parse_args()
 
 
-def shape_for(args) -> g.Shape:
-    if args.config == "mini":
-        s = g.MINI
-    elif args.config == "sweep":
-        s = g.SWEEP
-    else:  # one flash-shaped layer stack that fits HBM at C = E
-        s = g.Shape("flash1", 256, 8, 4096, 1024, 8, 32)
-    if args.layers:
-        s = g.Shape(s.name, s.num_experts, s.top_k, s.hidden, s.ffn, args.layers, s.tokens,
+SHAPES = {"mini": g.MINI, "sweep": g.SWEEP, "flash": g.FLASH,
+          "flash1": g.Shape("flash1", 256, 8, 4096, 1024, 8, 32)}
+
+
+def shape_for(name: str, layers: int = 0) -> g.Shape:
+    s = SHAPES[name]
+    if layers:
+        s = g.Shape(s.name, s.num_experts, s.top_k, s.hidden, s.ffn, layers, s.tokens,
                     s.steps, s.interval, s.capacity, s.dtype, s.shared_expert)
     return s
 
 
-def workload_str(s: g.Shape, cap: int, interval: int) -> str:
-    return (f"{s.name}: LLaDA2.0-{'mini' if s.hidden == 2048 else 'flash'}-shaped MoE stack, "
-            f"{s.layers} layers, E={s.num_experts} top-{s.top_k}"
-            f"{' + shared expert' if s.shared_expert else ''}, H={s.hidden}, F={s.ffn}, "
-            f"{s.tokens} tokens per layer-step ({s.tokens // 32} block(s) of 32), "
-            f"capacity {cap}{' (all experts in HBM)' if cap == s.num_experts else ' (pinned-host serving)'}, "
-            f"refresh interval {interval}, T={s.steps} steps per block")
+def workload_str(s: g.Shape, cap: int, interval: int, ep_world: int = 0) -> str:
+    kind = "mini" if s.hidden == 2048 else "flash"
+    if ep_world:
+        where = (f"expert parallel over {ep_world} GPU(s), {s.num_experts // ep_world} experts "
+                 f"per rank, capacity {cap} per rank")
+    else:
+        where = (f"capacity {cap}" + (" (all experts in HBM)" if cap == s.num_experts
+                                      else " (pinned-host serving)"))
+    return (f"{s.name}: LLaDA2.0-{kind}-shaped MoE stack, {s.layers} layers, E={s.num_experts} "
+            f"top-{s.top_k}{' + shared expert' if s.shared_expert else ''}, H={s.hidden}, "
+            f"F={s.ffn}, {s.tokens} tokens per layer-step per rank ({s.tokens // 32} block(s) "
+            f"of 32), {where}, refresh interval {interval}, T={s.steps} steps per block")
 
 
 # ------------------------------------------------------------------ clocks
@@ -106,7 +135,7 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -193,7 +222,7 @@ def _cpu_model() -> str:
     return f"{os.cpu_count()} logical CPUs"
 
 
-# ------------------------------------------------------------------ main arm
+# ------------------------------------------------------------------ helpers
 def h2d_peak_gbs(dev, mb: int = 256, reps: int = 5) -> float:
     """Pinned-host -> HBM copy bandwidth (best of `reps` copies of `mb` MB, CUDA events):
     the PCIe roofline for the pinned-host serving path (a6, SURVEY 8(d) metric 4)."""
@@ -211,251 +240,259 @@ def h2d_peak_gbs(dev, mb: int = 256, reps: int = 5) -> float:
     return best
 
 
-def max_over_ranks(v: float, world: int, dev) -> float:
-    """MAX over ranks of a device-timed value (NCCL: device tensor; gloo test mode: host)."""
+def reduce_over_ranks(v: float, world: int, dev, op="max") -> float:
+    """MAX (or MIN) over ranks of a device-timed value (NCCL: device tensor; gloo: host)."""
     if world == 1:
         return v
     gloo = torch.distributed.get_backend() == "gloo"
-    tm = torch.tensor([v], device="cpu" if gloo else dev)
-    torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+    tm = torch.tensor([v], dtype=torch.float64, device="cpu" if gloo else dev)
+    torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX if op == "max"
+                                 else torch.distributed.ReduceOp.MIN)
     return float(tm.item())
 
 
-def run_tide(args, rank: int, world: int, local_rank: int):
+def gather_over_ranks(vec: list, world: int, dev) -> list:
+    if world == 1:
+        return [list(vec)]
+    gloo = torch.distributed.get_backend() == "gloo"
+    t = torch.tensor(vec, dtype=torch.float64, device="cpu" if gloo else dev)
+    out = [torch.empty_like(t) for _ in range(world)]
+    torch.distributed.all_gather(out, t)
+    return [o.cpu().tolist() for o in out]
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def traffic_for(key: str):
+    """ncu DRAM bytes per FFN launch for exactly this run configuration, else None."""
+    tp = os.path.join(ROOT, "profiles", "ffn_traffic.json")
+    try:
+        d = json.load(open(tp)).get(key)
+    except Exception:
+        return None, None
+    return (d["dram_bytes_per_launch"], d) if d else (None, None)
+
+
+def act_bytes(H, F, rows):
+    """Per FFN row: x gathered (2H) + h written and read (2*2F) + y written (4H)."""
+    return rows * (H * 2 + 2 * F * 2 + H * 4)
+
+
+def gen_layer(args, s: g.Shape, l: int, dev, desc, experts=None, host=False):
+    """One layer's (router, packed experts, packed shared expert) from the seeded generator,
+    packed by the product API (tide_pack_expert); `host` moves the experts to pinned host."""
     from paper_2605_20179_b200 import tide
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    s = shape_for(args)
-    E, k, H, F, N, Lyr = s.num_experts, s.top_k, s.hidden, s.ffn, s.tokens, s.layers
-    cap = args.capacity or E
-    pool_mode = cap < E
-    desc = tide.make_desc(E, k, H, F, N, tide.TIDE_BF16, shared_expert=s.shared_expert)
-    seed = args.seed + 1000 * rank  # each rank runs its own blocks (weak scaling)
-    ep = args.ep
-    El = E // world if ep else E
-    if ep:
-        cap = min(args.capacity or El, El)
-        pool_mode = False
-        uid = [tide.nccl_unique_id() if rank == 0 else None]
-        if world > 1:
-            torch.distributed.broadcast_object_list(uid, src=0)
+    wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev,
+                                       skew=0.0 if args.routing == "uniform" else g.SKEW,
+                                       experts=experts)
+    packed = tide.pack_layer(desc, wg, wu, wd)
+    del wg, wu, wd
+    shared = torch.cat([a.reshape(-1) for a in sh]).contiguous() if sh else None
+    if host:
+        hm = packed.cpu().pin_memory()
+        del packed
+        packed = hm
+    torch.cuda.empty_cache()
+    return wr, packed, shared
 
-    # weights: generated on the device (bit-identical to the host generator), packed by the
-    # product API (tide_pack_expert); one context per layer (EP: this rank's E/P experts)
-    layers = []
-    for l in range(Lyr):
-        wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, l, dev,
-                                           skew=0.0 if args.routing == "uniform" else g.SKEW)
-        if ep:
-            sl = slice(rank * El, (rank + 1) * El)
-            wg, wu, wd = wg[sl].contiguous(), wu[sl].contiguous(), wd[sl].contiguous()
-        packed = tide.pack_layer(desc, wg, wu, wd)
-        del wg, wu, wd
-        torch.cuda.empty_cache()
-        shared = torch.cat([a.reshape(-1) for a in sh]).contiguous() if sh else None
-        w = {"device_all": packed} if not pool_mode else {"host_master": packed.cpu().pin_memory()}
-        if pool_mode:
-            del packed
-        if ep and args.p2p:
-            ctx = tide.EPPeerContext(desc, rank, world, local_rank)
-            hs = [None] * world
-            mine = ctx.export()
-            if world > 1:
-                torch.distributed.all_gather_object(hs, mine[0])
-                ctx.connect(handles=hs)
-                torch.distributed.barrier()
+
+# ------------------------------------------------------------------ the stack
+class Stack:
+    """One rank's MoE stack: per layer a context, weights, router, inputs for T steps.
+    mode: device_all | host_master | ep."""
+
+    def __init__(self, args, s: g.Shape, dev, rank: int, world: int, cap: int, mode: str,
+                 weights=None, p2p=False):
+        from paper_2605_20179_b200 import tide
+        self.tide, self.args, self.s, self.dev = tide, args, s, dev
+        self.rank, self.world, self.mode, self.p2p = rank, world, mode, p2p
+        E, k, H, F, N = s.num_experts, s.top_k, s.hidden, s.ffn, s.tokens
+        self.El = E // world if mode == "ep" else E
+        self.cap = cap
+        self.desc = tide.make_desc(E, k, H, F, N, tide.TIDE_BF16, shared_expert=s.shared_expert)
+        uni = args.routing == "uniform"
+        seed_x = args.seed + 1000 * rank  # each rank runs its own blocks (weak scaling)
+        self.layers = []
+        for l in range(s.layers):
+            if weights is not None:
+                wr, w, shared = weights[l]
             else:
-                ctx.connect(bases=[mine[1]])
-        elif ep:
-            ctx = tide.EPContext(desc, uid[0] if l == 0 else None, rank, world, local_rank,
-                                 like=None if l == 0 else layers[0]["ctx"])
-        else:
-            ctx = tide.Context(desc, cap, 16, local_rank)
-        layers.append(dict(router=wr, w=w, shared=shared, ctx=ctx,
-                           x=g.block_hidden_torch(s, seed, l, dev, iid=args.routing == "uniform"),
-                           pl=torch.zeros(El, dtype=torch.uint8, device=dev),
-                           hits=torch.empty(E, dtype=torch.int32, device=dev),
-                           out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
-    torch.cuda.synchronize()
-    T = s.steps
-    # NEXT-3: each layer prefetches the next layer's likely experts into L2 (ring: the
-    # last layer prefetches layer 0 for the next step)
-    pf_mb = args.prefetch_mb if args.prefetch_mb >= 0 else (32.0 if not pool_mode and not ep else 0.0)
-    if pf_mb > 0 and not pool_mode and not ep:
-        for li, L in enumerate(layers):
-            nx = layers[(li + 1) % Lyr]
-            L["ctx"].set_prefetch(nx["ctx"], nx["w"]["device_all"], int(pf_mb * 1e6))
+                ids = range(rank * self.El, (rank + 1) * self.El) if mode == "ep" else None
+                wr, w, shared = gen_layer(args, s, l, dev, self.desc, ids,
+                                          host=mode == "host_master")
+            if mode == "ep" and p2p:
+                ctx = tide.EPPeerContext(self.desc, rank, world, dev.index)
+            elif mode == "ep":
+                first = self.layers[0]["ctx"] if l else None
+                uid = None
+                if first is None:
+                    uid = [tide.nccl_unique_id() if rank == 0 else None]
+                    if world > 1:
+                        torch.distributed.broadcast_object_list(uid, src=0)
+                    uid = uid[0]
+                ctx = tide.EPContext(self.desc, uid, rank, world, dev.index, like=first)
+            else:
+                ctx = tide.Context(self.desc, cap, 16, dev.index)
+            self.layers.append(dict(router=wr, w=w, shared=shared, ctx=ctx,
+                                    x=g.block_hidden_torch(s, seed_x, l, dev, iid=uni),
+                                    pl=torch.zeros(self.El, dtype=torch.uint8, device=dev),
+                                    hits=torch.empty(E, dtype=torch.int32, device=dev),
+                                    out=torch.empty(N, H, dtype=torch.bfloat16, device=dev)))
+        if mode == "ep" and p2p:
+            self._connect()
+        torch.cuda.synchronize()
+        self.graphs = None
 
-    def layer_step(L, t, x=None, stats=False):
+    def weights(self):
+        return [(L["router"], L["w"], L["shared"]) for L in self.layers]
+
+    def _connect(self):
+        for L in self.layers:
+            ctx = L["ctx"]
+            h, base = ctx.export()
+            if self.world > 1:
+                hs = [None] * self.world
+                torch.distributed.all_gather_object(hs, h)
+                ctx.connect(handles=hs)
+            else:
+                ctx.connect(bases=[base])
+        if self.world > 1:
+            torch.distributed.barrier()
+
+    def set_prefetch(self, mb: float):
+        Ly = len(self.layers)
+        for li, L in enumerate(self.layers):
+            nx = self.layers[(li + 1) % Ly]
+            L["ctx"].set_prefetch(nx["ctx"] if mb > 0 else None, nx["w"] if mb > 0 else None,
+                                  int(mb * 1e6))
+
+    def layer_step(self, L, t, x=None, stats=False):
         xx = L["x"][t] if x is None else x
-        if ep:
-            return L["ctx"].moe_step_ep(xx, L["router"], L["w"]["device_all"],
-                                        shared_w=L["shared"], placement=L["pl"], step=t,
-                                        interval=args.interval, capacity=cap, out=L["out"],
-                                        hit_counts=L["hits"], placement_out=L["pl"], stats=stats)
-        return L["ctx"].moe_step(xx, L["router"], **L["w"],
-                                 shared_w=L["shared"], placement=L["pl"], step=t,
-                                 interval=args.interval, out=L["out"], hit_counts=L["hits"],
+        a = self.args
+        if self.mode == "ep":
+            return L["ctx"].moe_step_ep(xx, L["router"], L["w"], shared_w=L["shared"],
+                                        placement=L["pl"], step=t, interval=a.interval,
+                                        capacity=self.cap, out=L["out"], hit_counts=L["hits"],
+                                        placement_out=L["pl"], stats=stats)
+        wk = {"device_all": L["w"]} if self.mode == "device_all" else {"host_master": L["w"]}
+        return L["ctx"].moe_step(xx, L["router"], **wk, shared_w=L["shared"], placement=L["pl"],
+                                 step=t, interval=a.interval, out=L["out"], hit_counts=L["hits"],
                                  placement_out=L["pl"], stats=stats)
 
-    graphs = None
-
-    def bench_step(i, eager=False):
-        t = i % T
-        if graphs is not None and not eager:
-            graphs[t].replay()
+    def step(self, i, eager=False):
+        t = i % self.s.steps
+        if self.graphs is not None and not eager:
+            self.graphs[t].replay()
             return
-        for L in layers:
-            layer_step(L, t)
+        for L in self.layers:
+            self.layer_step(L, t)
 
-    for i in range(args.warmup):
-        bench_step(i)
-    torch.cuda.synchronize()
-    if not args.eager and not pool_mode and (not ep or args.p2p):  # NEXT-3: one graph per block step t, every layer-step of the stack in it
+    def reset(self):
+        for L in self.layers:
+            L["pl"].zero_()
+
+    def capture(self, warmup):
+        """NEXT-3: one CUDA graph per block step t, every layer-step of the stack in it."""
         gl = []
-        for t in range(T):
+        for t in range(self.s.steps):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
-                for L in layers:
-                    layer_step(L, t)
+                for L in self.layers:
+                    self.layer_step(L, t)
             gl.append(gr)
         torch.cuda.synchronize()
-        graphs = gl
-        for i in range(args.warmup):  # placement state continues from the eager warm-up
-            bench_step(args.warmup + i)
+        self.graphs = gl
+        for i in range(warmup):  # placement state continues from the eager warm-up
+            self.step(warmup + i)
         torch.cuda.synchronize()
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def timed_region(phase_timing: bool):
-        for L in layers:
+    def timed(self, steps, warmup, phase_timing=False):
+        for L in self.layers:
             L["ctx"].set_timing(phase_timing)
-        if world > 1:
+        if self.world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        for i in range(args.steps):
-            bench_step(args.warmup + i, eager=phase_timing)
+        for i in range(steps):
+            self.step(warmup + i, eager=phase_timing)
         e1.record(st)
         torch.cuda.synchronize()
-        t = e0.elapsed_time(e1)
-        if world > 1:
-            t = max_over_ranks(t, world, dev)
-        ph = [L["ctx"].timing() for L in layers] if phase_timing else None
-        for L in layers:
+        ms = reduce_over_ranks(e0.elapsed_time(e1), self.world, self.dev)
+        ph = [L["ctx"].timing() for L in self.layers] if phase_timing else None
+        for L in self.layers:
             L["ctx"].set_timing(False)
-        return t, ph
+        return ms, ph
 
-    # region 1: the headline number (no per-phase events in the stream)
-    clk = Clocks(local_rank)
-    ms, _ = timed_region(False)
-    clocks = clk.stop()
-    # region 2: same steps with per-phase CUDA events on the launching stream (roofline)
-    ms_phased, phases = timed_region(True)
-    # region 3: each step timed alone (events between steps): refresh vs skipped steps
-    # (SURVEY 8(d) metric 1; a step is a refresh step iff t % interval == 0)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        evs[i][0].record(st)
-        bench_step(args.warmup + i)
-        evs[i][1].record(st)
-    torch.cuda.synchronize()
-    per = [(a.elapsed_time(b), (args.warmup + i) % T % args.interval == 0)
-           for i, (a, b) in enumerate(evs)]
-    ref_ms = [m for m, r in per if r]
-    skp_ms = [m for m, r in per if not r]
-    step_split = {"ms_refresh_step": round(sum(ref_ms) / max(1, len(ref_ms)), 4),
-                  "ms_skipped_step": round(sum(skp_ms) / max(1, len(skp_ms)), 4),
-                  "refresh_steps": len(ref_ms), "skipped_steps": len(skp_ms),
-                  "p50_ms_step": round(float(np.percentile([m for m, _ in per], 50)), 4),
-                  "p90_ms_step": round(float(np.percentile([m for m, _ in per], 90)), 4)}
-    layer_steps = args.steps * Lyr
-    value = N * layer_steps * world / (ms / 1e3)
+    def step_split(self, steps, warmup):
+        """Each step timed alone: refresh (t % interval == 0) vs skipped steps (8(d) metric 1)."""
+        st = torch.cuda.current_stream()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        torch.cuda.synchronize()
+        for i in range(steps):
+            evs[i][0].record(st)
+            self.step(warmup + i)
+            evs[i][1].record(st)
+        torch.cuda.synchronize()
+        per = [(a.elapsed_time(b), (warmup + i) % self.s.steps % self.args.interval == 0)
+               for i, (a, b) in enumerate(evs)]
+        ref = [m for m, r in per if r]
+        skp = [m for m, r in per if not r]
+        return {"ms_refresh_step": round(sum(ref) / max(1, len(ref)), 4),
+                "ms_skipped_step": round(sum(skp) / max(1, len(skp)), 4),
+                "refresh_steps": len(ref), "skipped_steps": len(skp),
+                "p50_ms_step": round(float(np.percentile([m for m, _ in per], 50)), 4),
+                "p90_ms_step": round(float(np.percentile([m for m, _ in per], 90)), 4)}
 
-    # algorithmic FFN bytes of exactly the timed (layer, t) sequence: replay with stats
-    # (untimed; routing is deterministic, so the same experts are hit)
-    for L in layers:
-        L["pl"].zero_()
-    for i in range(args.warmup):
-        for L in layers:
-            layer_step(L, i % T)
-    ffn_bytes, uniq, w_read, copies, h2d = 0, 0, 0, 0, 0
-    R = N * k + (N if s.shared_expert else 0)
-    act_bytes = R * (H * 2 + 2 * F * 2 + H * 4)
-    for i in range(args.steps):
-        for L in layers:
-            r = layer_step(L, (args.warmup + i) % T, stats=True)
-            u = r.stats["unique_experts"] + (1 if s.shared_expert else 0)
-            uniq += u
-            w_read += r.stats["weight_bytes_read"]
-            if ep:  # this rank's local experts over every rank's rows
-                pairs = r.stats["resident_pairs"] + r.stats["nonresident_pairs"]
-                rows = pairs + (N if s.shared_expert else 0)
-                ffn_bytes += u * s.expert_bytes + rows * (H * 2 + 2 * F * 2 + H * 4)
-            else:
-                ffn_bytes += u * s.expert_bytes + act_bytes
-            copies += r.stats["copies"]
-            h2d += r.stats["h2d_bytes"]
-    ffn_ms = sum(p["ffn_ms"] for p in phases)
-    ffn_launches = sum(p["ffn_launches"] for p in phases)
-    launches = sum(p["launches"] for p in phases)
-    tot = {kk: sum(p[kk] for p in phases) for kk in ("router_ms", "route_ms", "gather_ms",
-                                                      "ffn_ms", "staged_ms", "combine_ms",
-                                                      "total_ms")}
-    # the resident FFN launch is one per layer-step: its bytes per launch
-    per_launch_bytes = ffn_bytes / layer_steps
-    ffn_avg_s = (tot["ffn_ms"] / 1e3) / layer_steps
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
-        "fallback 6.65 TB/s (B200_PROFILING.md)"
-    achieved = per_launch_bytes / ffn_avg_s / 1e9
-    traffic, traffic_detail = None, None
-    tp = os.path.join(ROOT, "profiles", "ffn_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic_detail = json.load(open(tp)).get(s.name)
-            traffic = traffic_detail["dram_bytes_per_launch"] if traffic_detail else None
-        except Exception:
-            traffic, traffic_detail = None, None
-    flops_per_layer_step = 2 * N * k * 3 * H * F + (2 * N * 3 * H * F if s.shared_expert else 0)
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
-                "traffic_detail": traffic_detail,
-                "kernel": "tide_ffn_kernel (grouped SwiGLU, tcgen05 + TMA)",
-                "peak_source": peak_src,
-                "bytes_per_launch": round(per_launch_bytes),
-                "avg_launch_us": round(ffn_avg_s * 1e6, 2),
-                "ffn_share_of_step": round(tot["ffn_ms"] / max(tot["total_ms"], 1e-9), 4),
-                "tensor_frac": round(flops_per_layer_step / ffn_avg_s / 1e12 /
-                                     peaks.get("bf16_tflops", 1590.0), 5),
-                "unique_experts_per_layer_step": round(uniq / layer_steps, 2)}
+    def stats_replay(self, steps, warmup):
+        """Replay exactly the timed (layer, t) sequence eagerly with stats (untimed; routing is
+        deterministic, so the same experts are hit) -> per-launch algorithmic bytes."""
+        s = self.s
+        self.reset()
+        for i in range(warmup):
+            for L in self.layers:
+                self.layer_step(L, i % s.steps)
+        acc = dict(alg=0, res_alg=0, uniq=0, copies=0, h2d=0, streamed=0, launches=0)
+        sh = 1 if s.shared_expert else 0
+        for i in range(steps):
+            for L in self.layers:
+                r = self.layer_step(L, (warmup + i) % s.steps, stats=True).stats
+                u = r["unique_experts"] + sh
+                acc["uniq"] += u
+                rows_all = r["resident_pairs"] + r["nonresident_pairs"] + (s.tokens if sh else 0)
+                acc["alg"] += u * s.expert_bytes + act_bytes(s.hidden, s.ffn, rows_all)
+                # resident launch: hit experts whose weights were in HBM at step start (+ shared)
+                acc["res_alg"] += ((u - r["experts_streamed"]) * s.expert_bytes
+                                   + act_bytes(s.hidden, s.ffn, r["resident_rows"]))
+                acc["copies"] += r["copies"]
+                acc["h2d"] += r["h2d_bytes"]
+                acc["streamed"] += r["experts_streamed"]
+                acc["launches"] += r["ffn_launches"]
+        return acc
 
-    # e2e: hidden states from pinned host in, output to pinned host out, every layer-step
-    e2e = None
-    if not args.no_e2e:
-        Ly = len(layers)
-        # inputs of step t for every layer contiguous in pinned host memory: layer 0's input
-        # goes first, layers 1.. in one copy that lands while layer 0 computes
-        xh = torch.stack([L["x"] for L in layers], 1).cpu().pin_memory()  # [T, L, N, H]
-        oh = [torch.empty(N, H, dtype=torch.bfloat16).pin_memory() for _ in layers]
+    def e2e(self, steps, warmup, graphs: bool):
+        """Same metric through the public API with every layer-step's hidden states copied
+        H2D from pinned host and its output D2H, on a copy stream that overlaps the transfers
+        with the layer-steps; captured in per-step graphs like the headline when it uses them."""
+        s, dev = self.s, self.dev
+        N, H = s.tokens, s.hidden
+        Ly = len(self.layers)
+        xh = torch.stack([L["x"] for L in self.layers], 1).cpu().pin_memory()  # [T, L, N, H]
+        oh = [torch.empty(N, H, dtype=torch.bfloat16).pin_memory() for _ in self.layers]
         xd = torch.empty(Ly, N, H, dtype=torch.bfloat16, device=dev)
-        cs = torch.cuda.Stream(device=dev)  # copy stream: PCIe transfers overlap the layer-steps
+        cs = torch.cuda.Stream(device=dev)
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_out = [torch.cuda.Event() for _ in layers]
+        ev_out = [torch.cuda.Event() for _ in self.layers]
 
         def e2e_step(t):
-            # the step's inputs go H2D on the copy stream (after the previous step's compute has
-            # consumed the buffers); each layer-step's output goes D2H on the copy stream while
-            # the next layer-step runs
-            ms = torch.cuda.current_stream()  # the capture stream under torch.cuda.graph
+            ms = torch.cuda.current_stream()
             cs.wait_stream(ms)
             with torch.cuda.stream(cs):
                 xd[0].copy_(xh[t, 0], non_blocking=True)
@@ -463,104 +500,396 @@ def run_tide(args, rank: int, world: int, local_rank: int):
                 if Ly > 1:
                     xd[1:].copy_(xh[t, 1:], non_blocking=True)
                     ev_in[1].record(cs)
-            for li, L in enumerate(layers):
+            for li, L in enumerate(self.layers):
                 if li < 2:
                     ms.wait_event(ev_in[li])
-                layer_step(L, t, x=xd[li])
+                self.layer_step(L, t, x=xd[li])
                 ev_out[li].record(ms)
                 cs.wait_event(ev_out[li])
                 with torch.cuda.stream(cs):
                     oh[li].copy_(L["out"], non_blocking=True)
             ms.wait_stream(cs)
 
-        e2e_graphs = None
-        if graphs is not None:  # same launch mode as the headline: copies captured in the graphs
-            e2e_graphs = []
-            for t in range(T):
+        gl = None
+        if graphs:
+            gl = []
+            for t in range(s.steps):
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr):
                     e2e_step(t)
-                e2e_graphs.append(gr)
-            for i in range(args.warmup):
-                e2e_graphs[(args.warmup + i) % T].replay()
-        if world > 1:
+                gl.append(gr)
+            for i in range(warmup):
+                gl[(warmup + i) % s.steps].replay()
+        if self.world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        for i in range(args.steps):
-            t = (args.warmup + i) % T
-            if e2e_graphs is not None:
-                e2e_graphs[t].replay()
+        for i in range(steps):
+            t = (warmup + i) % s.steps
+            if gl is not None:
+                gl[t].replay()
             else:
                 e2e_step(t)
         e1.record(st)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            ems = max_over_ranks(ems, world, dev)
-        e2e = {"value": N * layer_steps * world / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": Lyr * N * H * 2, "d2h_bytes_per_step": Lyr * N * H * 2,
-               "ms_per_step": ems / args.steps,
-               "launch": "CUDA graph per block step (copies captured)" if e2e_graphs else "eager",
-               "note": "tide_moe_step through the C ABI; per layer-step the block's hidden "
-                       "states are copied from pinned host and the output back, on a copy "
-                       "stream that overlaps the transfers with the layer-steps"}
-        del e2e_graphs
+        ems = reduce_over_ranks(e0.elapsed_time(e1), self.world, dev)
+        del gl
+        return {"value": round(N * steps * Ly * self.world / (ems / 1e3), 1), "unit": UNIT,
+                "h2d_bytes_per_step": Ly * N * H * 2, "d2h_bytes_per_step": Ly * N * H * 2,
+                "ms_per_step": round(ems / steps, 4),
+                "launch": "CUDA graph per block step (copies captured)" if graphs else "eager",
+                "note": "per layer-step the block's hidden states are copied from pinned host "
+                        "and the output back (per rank), on a copy stream that overlaps the "
+                        "transfers with the layer-steps"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
-        cpu = cpu_baseline(s, args.seed, args.cpu_seconds, min(N, 32), args.routing)
+    def close(self):
+        self.graphs = None
+        for L in self.layers:
+            L["ctx"].close()
 
-    io = None
-    if pool_mode:  # a6: the H2D link is the roofline of capacity-limited steps
-        pk = h2d_peak_gbs(dev)
-        eff = (h2d / args.steps) / (ms / args.steps / 1e3) / 1e9
-        io = {"copies_per_step": copies / args.steps, "h2d_bytes_per_step": h2d / args.steps,
-              "h2d_gbs_effective": round(eff, 2), "h2d_peak_gbs": round(pk, 2),
-              "frac": round(eff / pk, 4),
-              "note": "effective = expert bytes copied H2D per step / device time per step; "
-                      "peak = best pinned-host -> HBM copy of 256 MB measured in this run"}
-    res = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-           "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and " +
-                   ("calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)"
-                    if args.routing == "calibrated" else
-                    "uniform iid stress routing (alpha=0, a0=0, skew=0)"),
-           "config": {"workload": workload_str(s, cap, args.interval), "layers": Lyr,
-                      "tokens_per_layer_step": N, "num_experts": E, "top_k": k, "hidden": H,
-                      "ffn": F, "capacity": cap, "interval": args.interval,
-                      "routing": args.routing,
-                      "parallelism": (f"expert parallel x{world} (E/P = {El} experts per rank, "
-                                      + ("peer-memory dispatch/combine kernels)" if args.p2p else
-                                         "NCCL all-gather dispatch + all-to-all combine)")) if ep
-                      else f"replicas x{world} (each rank its own blocks)",
-                      "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
-                            "through the stack between reuses",
-                      "launch": ("CUDA graph per block step (all layers), replayed" if graphs
-                                 else "eager stream (PDL-chained kernels)"),
-                      "prefetch_mb": pf_mb},
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": launches * world if rank == 0 else launches,
-           "clocks": clocks,
+
+def phase_sums(phases):
+    keys = ("router_ms", "route_ms", "gather_ms", "ffn_ms", "staged_ms", "combine_ms", "total_ms")
+    return {kk: sum(p[kk] for p in phases) for kk in keys}, sum(p["launches"] for p in phases)
+
+
+# ------------------------------------------------------------------ single device
+def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=None, full=True,
+                   steps=None, warmup=None):
+    """One single-device (or replica) run of stack `s` at capacity `cap`: value, roofline
+    and, with `full`, clocks / e2e / step split / the prefetch-off control."""
+    steps = steps or args.steps
+    warmup = warmup or args.warmup
+    E, N, H, F = s.num_experts, s.tokens, s.hidden, s.ffn
+    pool = cap < E
+    st = Stack(args, s, dev, rank, world, cap, "host_master" if pool else "device_all",
+               weights=weights)
+    pf_mb = args.prefetch_mb if args.prefetch_mb >= 0 else (32.0 if not pool else 0.0)
+    if pf_mb > 0 and not pool:
+        st.set_prefetch(pf_mb)
+    for i in range(warmup):
+        st.step(i)
+    torch.cuda.synchronize()
+    graphs = not args.eager and not pool
+    if graphs:
+        st.capture(warmup)
+    clk = Clocks(dev.index) if full else None
+    ms, _ = st.timed(steps, warmup)
+    clocks = clk.stop() if clk else None
+    ms_ph, phases = st.timed(steps, warmup, phase_timing=True)
+    tot, launches = phase_sums(phases)
+    layer_steps = steps * s.layers
+    value = N * layer_steps * world / (ms / 1e3)
+    res = {"value": round(value, 1), "unit": UNIT, "ms_per_step": round(ms / steps, 4),
+           "us_per_layer_step": round(1e3 * ms / layer_steps, 2),
+           "workload": workload_str(s, cap, args.interval),
+           "launch": "CUDA graph per block step (all layers), replayed" if graphs
+                     else "eager stream (PDL-chained kernels)",
+           "prefetch_mb": pf_mb, "gpu_launches": launches, "steps": steps, "warmup": warmup,
            "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()},
-           "ms_per_step_with_phase_events": round(ms_phased / args.steps, 4),
-           "step_split": step_split,
-           "io": io}
+           "ms_per_step_with_phase_events": round(ms_ph / steps, 4)}
+    if full:
+        res["clocks"] = clocks
+        res["step_split"] = st.step_split(steps, warmup)
+    acc = st.stats_replay(steps, warmup)
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    peak_src = ("measured (MEASURED_PEAKS.json hbm_gbs, device copy)" if "hbm_gbs" in pk
+                else "fallback 6.65 TB/s (B200_PROFILING.md)")
+    ffn_s = (tot["ffn_ms"] / 1e3) / layer_steps  # the first (resident) FFN launch of a step
+    if not pool:
+        per_launch = acc["alg"] / layer_steps
+        achieved = per_launch / ffn_s / 1e9
+        tkey = f"{s.name}|{args.routing}|C={cap}|ep=none|L={s.layers}"
+        traffic, tdet = traffic_for(tkey)
+        flops = 2 * N * s.top_k * 3 * H * F + (2 * N * 3 * H * F if s.shared_expert else 0)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
+                "kernel": "tide_ffn_kernel (grouped SwiGLU, tcgen05 + TMA)",
+                "peak_source": peak_src, "bytes_per_launch": round(per_launch),
+                "avg_launch_us": round(ffn_s * 1e6, 2),
+                "ffn_share_of_step": round(tot["ffn_ms"] / max(tot["total_ms"], 1e-9), 4),
+                "tensor_frac": round(flops / ffn_s / 1e12 / pk.get("bf16_tflops", 1590.0), 5),
+                "unique_experts_per_layer_step": round(acc["uniq"] / layer_steps, 2),
+                "traffic_key": tkey, "traffic_detail": tdet,
+                "l2_prefetch": (f"{pf_mb:g} MB of this layer's likely experts were prefetched "
+                                "into L2 by the previous layer's FFN tail (see "
+                                "frac_prefetch_off)" if pf_mb > 0 else "off")}
+        if full and pf_mb > 0:  # control: the same launches with the cross-layer prefetch off
+            st.set_prefetch(0)
+            _, ph0 = st.timed(steps, warmup, phase_timing=True)
+            t0, _ = phase_sums(ph0)
+            f0 = (t0["ffn_ms"] / 1e3) / layer_steps
+            roof["frac_prefetch_off"] = round(per_launch / f0 / 1e9 / peak, 4)
+            roof["avg_launch_us_prefetch_off"] = round(f0 * 1e6, 2)
+            st.set_prefetch(pf_mb)
+        res["roofline"] = roof
+    else:
+        pkh = h2d_peak_gbs(dev)
+        eff = (acc["h2d"] / steps) / (ms / steps / 1e3) / 1e9
+        res_launch = acc["res_alg"] / layer_steps
+        res["roofline"] = {
+            "bound": "pcie", "achieved": round(eff, 2), "peak": round(pkh, 2), "unit": "GB/s",
+            "frac": round(eff / pkh, 4), "traffic": None,
+            "kernel": "expert H2D copies (a6, cudaMemcpyAsync on the side stream)",
+            "peak_source": "best pinned-host -> HBM copy of 256 MB measured in this run",
+            "note": "capacity-limited steps are bound by the H2D link (SURVEY 8(d)): achieved = "
+                    "expert bytes copied H2D per step / device time per step",
+            "copies_per_step": round(acc["copies"] / steps, 2),
+            "h2d_bytes_per_step": round(acc["h2d"] / steps),
+            "ffn_resident_launch": {
+                "bytes_per_launch": round(res_launch),
+                "avg_launch_us": round(ffn_s * 1e6, 2),
+                "achieved_gbs": round(res_launch / ffn_s / 1e9, 1),
+                "frac_of_hbm_peak": round(res_launch / ffn_s / 1e9 / peak, 4),
+                "note": "the step's first FFN launch (experts in HBM at step start + shared) "
+                        "timed alone by events on its stream; the staged-chunk launches wait on "
+                        "their copies and are not in it"},
+            "ffn_launches_per_layer_step": round(acc["launches"] / layer_steps, 2)}
+    if full and not args.no_e2e:
+        res["e2e"] = st.e2e(steps, warmup, graphs)
+    st.close()
+    del st
+    torch.cuda.empty_cache()
     return res
 
 
-def run_reference(args):
+def sub_results(args, dev):
+    """N=1 companions of the headline, each a full pass of the hot path measured the same
+    way (graphs when every expert is in HBM): BJ.configs[4] the 8-block sweep batch at C = E
+    (the mini stack's weights, 256 tokens per layer-step), and BJ.configs[2] the flash-shaped
+    stack with pinned-host serving at the paper's budget C = 64 and at C = 217 (8 of its 32
+    layers: 206 GB of experts do not fit one GPU)."""
+    from paper_2605_20179_b200 import tide
+    out = {}
+    steps, warmup = min(args.steps, 20), max(3, min(args.warmup, 5))
+    try:
+        sw = shape_for("sweep")
+        desc = tide.make_desc(sw.num_experts, sw.top_k, sw.hidden, sw.ffn, sw.tokens,
+                              tide.TIDE_BF16, shared_expert=True)
+        w = [gen_layer(args, sw, l, dev, desc) for l in range(sw.layers)]
+        out["sweep_8blocks_C256"] = measure_single(args, sw, 256, dev, weights=w, full=False,
+                                                   steps=steps, warmup=warmup)
+        del w
+    except Exception as e:  # reported, not hidden
+        out["sweep_8blocks_C256"] = {"error": repr(e)[:300]}
+    torch.cuda.empty_cache()
+    try:
+        fs = shape_for("flash1")
+        desc = tide.make_desc(fs.num_experts, fs.top_k, fs.hidden, fs.ffn, fs.tokens,
+                              tide.TIDE_BF16)
+        w = [gen_layer(args, fs, l, dev, desc, host=True) for l in range(fs.layers)]
+        for cap in (64, 217):
+            out[f"flash_C{cap}_8layers"] = measure_single(args, fs, cap, dev, weights=w,
+                                                          full=False, steps=max(3, steps // 2),
+                                                          warmup=warmup)
+        del w
+    except Exception as e:
+        out["flash_pinned_host"] = {"error": repr(e)[:300]}
+    torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------------ expert parallel
+def ep_pair_counts(st: Stack, steps, warmup):
+    """[P] number of this rank's (token, slot) pairs routed to each rank's experts over the
+    timed (layer, t) sequence, for NVLink byte accounting only (an fp32 torch evaluation of
+    the router; a near-tie token may land one pair on a different rank than the kernel's)."""
+    s = st.s
+    cnt = np.zeros(st.world, np.int64)
+    for i in range(steps):
+        t = (warmup + i) % s.steps
+        for L in st.layers:
+            lg = L["x"][t].float() @ L["router"].float().T
+            top = torch.topk(lg, s.top_k, dim=1).indices
+            cnt += np.bincount((top // st.El).flatten().cpu().numpy(), minlength=st.world)
+    return cnt
+
+
+def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full=True):
+    E, N, H, k = s.num_experts, s.tokens, s.hidden, s.top_k
+    El = E // world
+    cap = min(args.capacity or El, El)
+    st = Stack(args, s, dev, rank, world, cap, "ep", weights=weights, p2p=p2p)
+    steps, warmup = args.steps, args.warmup
+    for i in range(warmup):
+        st.step(i)
+    torch.cuda.synchronize()
+    graphs = not args.eager
+    if graphs:
+        try:
+            st.capture(warmup)
+        except Exception as e:  # capture unsupported in this setting: time eagerly, say so
+            st.graphs = None
+            graphs = False
+            print(f"bench: EP graph capture failed ({e!r}); eager launches", file=sys.stderr)
+    clk = Clocks(dev.index) if full else None
+    ms, _ = st.timed(steps, warmup)
+    clocks = clk.stop() if clk else None
+    if p2p:
+        errs = [L["ctx"].error() for L in st.layers]
+        if any(errs):
+            raise RuntimeError(f"peer-memory EP watchdog fired on rank {rank}: {errs}")
+    ms_ph, phases = st.timed(steps, warmup, phase_timing=True)
+    tot, launches = phase_sums(phases)
+    layer_steps = steps * s.layers
+    value = N * layer_steps * world / (ms / 1e3)
+    acc = st.stats_replay(steps, warmup)
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    ffn_s = (tot["ffn_ms"] / 1e3) / layer_steps
+    per_launch = acc["alg"] / layer_steps
+    ach = per_launch / ffn_s / 1e9
+    ach_min = reduce_over_ranks(ach, world, dev, op="min")
+    # NVLink bytes out of / into this rank per layer-step (SURVEY 8(d) metric 5)
+    cnt = ep_pair_counts(st, steps, warmup)
+    allc = gather_over_ranks(cnt.tolist(), world, dev)  # allc[src][dst] pairs
+    peers = world - 1
+    y_out = sum(allc[src][rank] for src in range(world) if src != rank) * H * 4 / layer_steps
+    y_in = sum(cnt[d] for d in range(world) if d != rank) * H * 4 / layer_steps
+    if p2p:
+        disp = peers * (N * H * 2 + N * k * 8 + 4)
+        out_b, in_b = disp + y_out + peers * El * 4, disp + y_in + peers * El * 4
+        how = ("kernel peer stores: X rows + top-k/gates to every peer (router), pair y rows "
+               "to their token's rank (FFN epilogue), local counts to every peer")
+    else:
+        out_b = in_b = peers * (N * (H * 2 + k * 8) + N * H * 4 + El * 4)
+        how = ("NCCL: all-gather of [x | top-k | gates] (max_tokens rows per rank), all-to-all "
+               "of fp32 partial sums (max_tokens rows per peer), all-gather of local counts")
+    lstep_s = ms / 1e3 / layer_steps
+    nv = {"bytes_out_per_layer_step": round(out_b), "bytes_in_per_layer_step": round(in_b),
+          "gbs_out": round(out_b / lstep_s / 1e9, 2), "peak_gbs": NVLINK_GBS,
+          "frac": round(out_b / lstep_s / 1e9 / NVLINK_GBS, 5), "how": how,
+          "note": "the rank's NVLink bytes per layer-step / layer-step time: an average over the "
+                  "step (a few MB per step are latency-bound, not a link-saturation test)"}
+    res = {"value": round(value, 1), "unit": UNIT, "ms_per_step": round(ms / steps, 4),
+           "us_per_layer_step": round(1e3 * ms / layer_steps, 2),
+           "workload": workload_str(s, cap, args.interval, ep_world=world),
+           "exchange": "peer memory (dispatch in the router, combine in the FFN epilogue)" if p2p
+                       else "NCCL collectives",
+           "launch": "CUDA graph per block step (all layers), replayed" if graphs
+                     else "eager stream",
+           "gpu_launches": launches,
+           "roofline": {"bound": "hbm", "achieved": round(ach_min, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(ach_min / peak, 4), "traffic": None,
+                        "kernel": "tide_ffn_kernel over the rank's local experts",
+                        "rank0_achieved": round(ach, 1) if rank == 0 else None,
+                        "note": "min over ranks of the FFN's algorithmic bytes per launch / its "
+                                "launch time",
+                        "bytes_per_launch": round(per_launch),
+                        "avg_launch_us": round(ffn_s * 1e6, 2)},
+           "nvlink": nv,
+           "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()}}
+    if full:
+        res["clocks"] = clocks
+        res["step_split"] = st.step_split(steps, warmup)
+        if not args.no_e2e:
+            res["e2e"] = st.e2e(steps, warmup, graphs)
+    w = st.weights()
+    st.close()
+    del st
+    torch.cuda.empty_cache()
+    return res, w
+
+
+# ------------------------------------------------------------------ arms
+def run_tide(args, rank: int, world: int, local_rank: int, nccl_ok: bool = True):
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ep = (args.ep or world > 1) and not args.replicas
+    name = args.config or ("flash" if ep and world > 1 else "mini")
+    s = shape_for(name, args.layers)
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and " +
+                    ("calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)"
+                     if args.routing == "calibrated" else
+                     "uniform iid stress routing (alpha=0, a0=0, skew=0)"),
+            "paper_context": PAPER_CONTEXT}
+    if ep:
+        E = s.num_experts
+        p2p = not args.nccl and (world > 1 or args.p2p)
+        try:
+            head, w = measure_ep(args, s, dev, rank, world, p2p)
+        except Exception as e:
+            if not p2p or not nccl_ok:
+                raise
+            print(f"bench: peer-memory EP failed on rank {rank} ({e!r}); NCCL EP is the "
+                  f"headline", file=sys.stderr)
+            head, w = measure_ep(args, s, dev, rank, world, False)
+            head["p2p_error"] = repr(e)[:300]
+            p2p = False
+        sub = {}
+        if p2p and nccl_ok and not args.no_sub:  # the NCCL variant on the same weights
+            try:
+                sub["nccl_ep"], _ = measure_ep(args, s, dev, rank, world, False, weights=w,
+                                               full=False)
+            except Exception as e:
+                sub["nccl_ep"] = {"error": repr(e)[:300]}
+        del w
+        res = dict(base, value=head.pop("value"), ms_per_step=head.pop("ms_per_step"),
+                   config={"workload": head.pop("workload"), "layers": s.layers,
+                           "tokens_per_layer_step_per_rank": s.tokens, "num_experts": E,
+                           "top_k": s.top_k, "hidden": s.hidden, "ffn": s.ffn,
+                           "capacity_per_rank": min(args.capacity or E // world, E // world),
+                           "interval": args.interval, "routing": args.routing,
+                           "parallelism": f"expert parallel x{world} (E/P = {E // world} experts "
+                                          f"per rank), {head.pop('exchange')}",
+                           "l2": "inputs larger than L2: each layer's local weights rotate "
+                                 "through the stack between reuses",
+                           "launch": head.pop("launch")},
+                   roofline=head.pop("roofline"), nvlink=head.pop("nvlink"),
+                   e2e=head.pop("e2e", None), clocks=head.pop("clocks", None),
+                   gpu_launches=int(head.pop("gpu_launches")) * world,
+                   cpu_baseline=None, sub_results=sub)
+        res.update(head)
+        if world == 1 and rank == 0 and not args.no_cpu:
+            res["cpu_baseline"] = cpu_baseline(s, args.seed, args.cpu_seconds, min(s.tokens, 32),
+                                               args.routing)
+        return res
+
+    cap = args.capacity or s.num_experts
+    head = measure_single(args, s, cap, dev, rank, world)
+    head.pop("steps"), head.pop("warmup")
+    res = dict(base, value=head.pop("value"), ms_per_step=head.pop("ms_per_step"),
+               config={"workload": head.pop("workload"), "layers": s.layers,
+                       "tokens_per_layer_step": s.tokens, "num_experts": s.num_experts,
+                       "top_k": s.top_k, "hidden": s.hidden, "ffn": s.ffn, "capacity": cap,
+                       "interval": args.interval, "routing": args.routing,
+                       "parallelism": f"replicas x{world} (each rank its own blocks)",
+                       "l2": "inputs larger than L2: each layer's weights (>=1.6 GB) rotate "
+                             "through the stack between reuses",
+                       "launch": head.pop("launch"), "prefetch_mb": head.pop("prefetch_mb")},
+               roofline=head.pop("roofline"), e2e=head.pop("e2e", None),
+               clocks=head.pop("clocks", None),
+               gpu_launches=int(head.pop("gpu_launches")) * world, cpu_baseline=None)
+    res.update(head)
+    if world == 1 and rank == 0 and not args.no_cpu:  # the CPU baseline is an N=1 figure
+        res["cpu_baseline"] = cpu_baseline(s, args.seed, args.cpu_seconds, min(s.tokens, 32),
+                                           args.routing)
+    if (world == 1 and not args.no_sub and args.config is None and not args.layers
+            and not args.capacity and args.routing == "calibrated"):
+        res["sub_results"] = sub_results(args, dev)
+    return res
+
+
+def run_reference(args, world: int):
     """Reference arm of this tier: the fp64 CPU oracle, as it stands, timed on every host core
     (OpenMP over tokens) on the bench workload's layer-steps (layer 0 of the stack, the
     block's full token count)."""
     import oracle
-    s = shape_for(args)
+    ep = (args.ep or world > 1) and not args.replicas
+    s = shape_for(args.config or ("flash" if ep and world > 1 else "mini"), args.layers)
     N = s.tokens
     uni = args.routing == "uniform"
     wr, wg, wu, wd, sh = g.layer_torch(s, args.seed, 0, "cpu", skew=0.0 if uni else g.SKEW)
     to = g.torch_to_np
     L = oracle.Layer(to(wr), to(wg), to(wu), to(wd), tuple(to(a) for a in sh) if sh else None)
+    del wg, wu, wd
     xs = g.block_hidden_np(s, args.seed, 0, steps=s.steps, tokens=N, iid=uni)
     E = s.num_experts
     cap = args.capacity or E
@@ -576,42 +905,73 @@ def run_reference(args):
     el = time.perf_counter() - t0
     v = N * args.steps / el
     sample = (f"each step = one full layer-step (router..combine, fp64, {cores} host threads, "
-              f"OpenMP over tokens) of layer 0 of the stack on all {N} tokens of the block")
+              f"OpenMP over tokens) of layer 0 of the stack on all {N} tokens of one block")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
-            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * el / args.steps, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_str(s, cap, args.interval), "layers": s.layers,
                        "tokens_per_layer_step": s.tokens, "num_experts": E, "top_k": s.top_k,
                        "hidden": s.hidden, "ffn": s.ffn, "capacity": cap,
                        "interval": args.interval, "routing": args.routing,
-                       "oracle_sample": f"layer 0 of {s.layers}, all {N} tokens per step"},
+                       "oracle_sample": f"layer 0 of {s.layers}, all {N} tokens per step, on "
+                                        f"rank 0 (the oracle has no multi-GPU form)"},
             "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample, "host_cpu": _cpu_model()},
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
+def _free_port() -> int:
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
+
+
+def spawn(args) -> int:
+    """`python bench.py --gpus N` without torchrun: launch N ranks through torchrun on this
+    node (one process per GPU); fails loudly when the node has fewer GPUs."""
+    n = torch.cuda.device_count()
+    if n < args.gpus and not os.environ.get("TIDE_BENCH_SAME_DEVICE"):
+        print(f"bench.py: --gpus {args.gpus} but this node has {n} CUDA device(s)", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(spawn(args))
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    # test mode for the multi-process code path on a one-GPU box: every rank on cuda:0 and a
-    # gloo process group (NCCL refuses two ranks on one device); only --ep --p2p and replicas
-    if os.environ.get("TIDE_BENCH_SAME_DEVICE"):
-        local_rank = 0
-    if args.impl == "reference":
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "reference":  # the oracle has no multi-GPU form: rank 0 alone
         if rank == 0:
-            print(json.dumps(run_reference(args)), flush=True)
+            print(json.dumps(run_reference(args, world)), flush=True)
         return
+    # test mode for the multi-process code path on a one-GPU box: every rank on cuda:0 and a
+    # gloo process group (NCCL refuses two ranks per device); replicas and peer-memory EP only
+    same_dev = bool(os.environ.get("TIDE_BENCH_SAME_DEVICE"))
+    if same_dev:
+        local_rank = 0
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # keep the NCCL init lines (comm size)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        if os.environ.get("TIDE_BENCH_SAME_DEVICE"):
+        if same_dev:
             torch.distributed.init_process_group("gloo")
         else:
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_tide(args, rank, world, local_rank)
+    res = run_tide(args, rank, world, local_rank, nccl_ok=not (same_dev and world > 1))
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

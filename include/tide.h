@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TIDE_ABI_VERSION 1
+#define TIDE_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define TIDE_API __attribute__((visibility("default")))
@@ -129,6 +129,11 @@ typedef struct {
   int32_t copies;             /* expert H2D copies enqueued this step (incl. eager promotions) */
   int64_t h2d_bytes;          /* copies * tide_expert_bytes                              */
   int64_t weight_bytes_read;  /* expert weight bytes the grouped FFN streamed from HBM   */
+  /* the first FFN launch of the step (experts whose weights were in HBM at step start,
+   * + the shared expert); host_master mode runs one more launch per staged chunk      */
+  int64_t resident_weight_bytes; /* weight bytes that launch streamed                  */
+  int32_t resident_rows;      /* token rows it computed (routed pairs + shared rows)     */
+  int32_t ffn_launches;       /* grouped-FFN launches of this step                       */
 } tide_step_stats;
 
 /* Optional device outputs for tests (nullable members, device pointers).  */
@@ -177,10 +182,15 @@ TIDE_API void tide_ctx_destroy(tide_ctx* ctx);
  *  placement_out : device [E] uint8, placement' (may alias `placement`).
  * Returns TIDE_EPLACEMENT when the step is not a refresh and the input
  * placement holds more than `capacity` experts.  That check runs on the
- * device: when it fails, the router/routing kernels (and hit_counts) have
- * run but nothing after them, and `out` / `placement_out` are not written.
- * In device_all mode (no offload) the check is reported only when `stats`
- * is requested (the call does not otherwise synchronise).
+ * device, in the bookkeeping kernel after the router: when it fails,
+ * hit_counts holds this step's hits, placement_out is a copy of the input
+ * placement (unchanged), and no bucket / pos / I/O work is done.  In
+ * device_all mode the FFN and combine still run (they compute every hit
+ * expert whatever the placement, so `out` holds the layer's output); in
+ * host_master mode the resident FFN has run, no H2D copy or staged FFN is
+ * enqueued and `out` is not valid.  In device_all mode (no offload) the
+ * status is reported only when `stats` is requested (the call does not
+ * otherwise synchronise); host_master mode always reports it.
  * In host_master mode the call blocks once on an internal event after the
  * routing kernels to read the <= E-entry miss list, then enqueues H2D copies
  * on an internal side stream, overlapped with the resident experts' FFN.   */

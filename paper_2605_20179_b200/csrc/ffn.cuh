@@ -506,10 +506,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if constexpr (EP) {  // every CTA's peer stores precede its gpu-scope arrival
+  if constexpr (EP) {  // every CTA fences its own peer y stores at system scope, then arrives
     __shared__ int s_last;
     if (threadIdx.x == 0) {
-      __threadfence();
+      __threadfence_system();
       s_last = atomicAdd(p.ep_done, 1) == (int)gridDim.x - 1;
     }
     __syncthreads();

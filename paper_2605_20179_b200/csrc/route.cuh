@@ -253,8 +253,11 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   __syncthreads();
   if (tid == 0) {
     if (tr) tr[1] = globaltimer_ns();
-    // release this CTA's logits (and EP peer stores: the grid's last CTA publishes them at
-    // system scope); acquire the earlier arrivals' for the group's phase 2
+    // EP: this CTA's peer stores (X slices) are made visible at system scope by the CTA
+    // itself (after the barrier, cumulative over the CTA's threads), not only through the
+    // gpu-scope arrival chain to the grid's last CTA
+    if (p.ep_P) __threadfence_system();
+    // release this CTA's logits; acquire the earlier arrivals' for the group's phase 2
     s_flag = atom_add_acq_rel_gpu(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
@@ -289,6 +292,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
+    if (p.ep_P) __threadfence_system();  // this CTA's peer top-k / gate stores (see above)
     if (atom_add_acq_rel_gpu(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
@@ -564,6 +568,10 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
     info_hits[e] = s_hits[e];
   }
   if (!p.refresh && s_cnt > p.capacity) {  // S:49, S:263 budget safety
+    for (int e = tid; e < E; e += blockDim.x) {  // placement' = the (unchanged) input
+      p.placement_out[e] = (uint8_t)s_pl[e];
+      info_pl[e] = (uint8_t)s_pl[e];
+    }
     for (int i = tid; i < E * NW; i += blockDim.x) p.mask_rw[i] = 0u;
     if (tid == 0) p.info->status = 3;
     return;

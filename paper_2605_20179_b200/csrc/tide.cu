@@ -248,14 +248,18 @@ static void touch(F* f) {
 static void preload_ep_p2p_kernels(const tide_ctx* c) {
   const int epl = route_epl(c->E);
   if (c->bf16 && c->E % 16 == 0 && c->H % 256 == 0) {
+    // both register budgets: launch_route picks MINB = 2 when the grid exceeds one wave
+#define TOUCH_TC(EP) \
+  do { touch(tide_route_tc_kernel<EP, 8, 1>); touch(tide_route_tc_kernel<EP, 8, 2>); } while (0)
     switch (epl) {
-      case 1: touch(tide_route_tc_kernel<1, 8, 1>); break;
-      case 2: touch(tide_route_tc_kernel<2, 8, 1>); break;
-      case 4: touch(tide_route_tc_kernel<4, 8, 1>); break;
-      case 8: touch(tide_route_tc_kernel<8, 8, 1>); break;
-      case 16: touch(tide_route_tc_kernel<16, 8, 1>); break;
-      default: touch(tide_route_tc_kernel<32, 8, 1>); break;
+      case 1: TOUCH_TC(1); break;
+      case 2: TOUCH_TC(2); break;
+      case 4: TOUCH_TC(4); break;
+      case 8: TOUCH_TC(8); break;
+      case 16: TOUCH_TC(16); break;
+      default: TOUCH_TC(32); break;
     }
+#undef TOUCH_TC
   }
 #define TOUCH_ROUTE(TT)                                     \
   switch (epl) {                                            \
@@ -635,35 +639,74 @@ tide_status tide_ctx_create_ep_like(const tide_layer_desc* d, tide_ctx* parent, 
   return ctx_create_ep_impl(d, parent->device, nullptr, parent, parent->rank, parent->world, out);
 }
 
-// Lazily set up host_master resources (slot pool, staging ring, pinned mirrors).
+// Lazily set up host_master resources (slot pool, staging ring, pinned mirrors).  Everything
+// is allocated into locals and committed to the context only when all of it succeeded, so a
+// failed call leaves the context as it was (the next call retries).
 static tide_status ensure_pool(tide_ctx* c) {
   if (c->pool) return TIDE_OK;
   const int slots = c->capacity + c->staging;
-  if (cudaMalloc(&c->pool, c->expert_bytes * slots) != cudaSuccess)
+  const int E = c->E;
+  const int max_chunks = E + 2, max_entries2 = E + (c->maxN * c->k) / kMaxTok + 2;
+  void* pool = nullptr;
+  int4* entries2 = nullptr;
+  int *ctrl2 = nullptr, *done2 = nullptr, *h_ctrl2 = nullptr, *h_slot_of = nullptr;
+  void* h_info = nullptr;
+  int4* h_entries2 = nullptr;
+  std::vector<cudaEvent_t> ready(max_chunks, nullptr), done(max_chunks, nullptr);
+  auto cleanup = [&]() {
+    void* dev[] = {pool, entries2, ctrl2, done2};
+    for (void* p : dev)
+      if (p) cudaFree(p);
+    void* host[] = {h_info, h_entries2, h_ctrl2, h_slot_of};
+    for (void* p : host)
+      if (p) cudaFreeHost(p);
+    for (cudaEvent_t e : ready)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : done)
+      if (e) cudaEventDestroy(e);
+  };
+  bool ok = cudaMalloc(&pool, c->expert_bytes * slots) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cleanup();
     return fail(TIDE_ENOMEM, "slot pool of %d experts (%zu B) failed", slots,
                 c->expert_bytes * slots);
-  c->owner.assign(slots, -1);
-  const int E = c->E;
-  c->max_chunks = E + 2;
-  c->max_entries2 = E + (c->maxN * c->k) / kMaxTok + 2;
-  CU_TRY(cudaMalloc(&c->entries2, sizeof(int4) * c->max_entries2));
-  CU_TRY(cudaMalloc(&c->ctrl2, sizeof(int) * 2 * c->max_chunks));
-  CU_TRY(cudaMalloc(&c->done2, sizeof(int) * c->max_entries2));
-  CU_TRY(cudaHostAlloc(&c->h_info, c->info_bytes, cudaHostAllocDefault));
-  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_entries2), sizeof(int4) * c->max_entries2,
-                       cudaHostAllocDefault));
-  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ctrl2),
-                       sizeof(int) * (2 * c->max_chunks + c->max_entries2), cudaHostAllocDefault));
-  CU_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_slot_of), sizeof(int) * E,
-                       cudaHostAllocDefault));
-  for (int i = 0; i < E; ++i) c->h_slot_of[i] = -1;
-  CU_TRY(cudaMemcpy(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice));
-  c->ev_chunk_ready.resize(c->max_chunks);
-  c->ev_chunk_done.resize(c->max_chunks);
-  for (int i = 0; i < c->max_chunks; ++i) {
-    CU_TRY(cudaEventCreateWithFlags(&c->ev_chunk_ready[i], cudaEventDisableTiming));
-    CU_TRY(cudaEventCreateWithFlags(&c->ev_chunk_done[i], cudaEventDisableTiming));
   }
+  ok = cudaMalloc(reinterpret_cast<void**>(&entries2), sizeof(int4) * max_entries2) == cudaSuccess &&
+       cudaMalloc(reinterpret_cast<void**>(&ctrl2), sizeof(int) * 2 * max_chunks) == cudaSuccess &&
+       cudaMalloc(reinterpret_cast<void**>(&done2), sizeof(int) * max_entries2) == cudaSuccess &&
+       cudaHostAlloc(&h_info, c->info_bytes, cudaHostAllocDefault) == cudaSuccess &&
+       cudaHostAlloc(reinterpret_cast<void**>(&h_entries2), sizeof(int4) * max_entries2,
+                     cudaHostAllocDefault) == cudaSuccess &&
+       cudaHostAlloc(reinterpret_cast<void**>(&h_ctrl2),
+                     sizeof(int) * (2 * max_chunks + max_entries2), cudaHostAllocDefault) == cudaSuccess &&
+       cudaHostAlloc(reinterpret_cast<void**>(&h_slot_of), sizeof(int) * E, cudaHostAllocDefault) ==
+           cudaSuccess;
+  for (int i = 0; ok && i < max_chunks; ++i)
+    ok = cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) == cudaSuccess;
+  if (ok) {
+    for (int i = 0; i < E; ++i) h_slot_of[i] = -1;
+    ok = cudaMemcpy(c->slot_of_dev, h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  if (!ok) {
+    cudaError_t e = cudaGetLastError();
+    cleanup();
+    return fail(TIDE_ENOMEM, "host_master resources: %s", cudaGetErrorString(e));
+  }
+  c->pool = pool;
+  c->entries2 = entries2;
+  c->ctrl2 = ctrl2;
+  c->done2 = done2;
+  c->h_info = h_info;
+  c->h_entries2 = h_entries2;
+  c->h_ctrl2 = h_ctrl2;
+  c->h_slot_of = h_slot_of;
+  c->max_chunks = max_chunks;
+  c->max_entries2 = max_entries2;
+  c->ev_chunk_ready = std::move(ready);
+  c->ev_chunk_done = std::move(done);
+  c->owner.assign(slots, -1);
   return TIDE_OK;
 }
 
@@ -781,7 +824,11 @@ static tide_status ensure_weight_maps(tide_ctx* c, const void* src, int rows_exp
 }
 
 static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, int copies,
-                       int64_t weight_bytes, tide_step_stats* st) {
+                       int64_t weight_bytes, tide_step_stats* st, int64_t resident_wb,
+                       int resident_rows, int ffn_launches) {
+  st->resident_weight_bytes = resident_wb;
+  st->resident_rows = resident_rows;
+  st->ffn_launches = ffn_launches;
   st->refreshed = info->refreshed;
   st->resident_pairs = info->resident_pairs;
   st->nonresident_pairs = N * c->k - info->resident_pairs;
@@ -934,7 +981,8 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
 // experts without hits after the hit ones.
 static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const RouteInfo* hinfo,
                              int N, cudaStream_t st, int* streamed, int* copies,
-                             int64_t* weight_bytes) {
+                             int64_t* weight_bytes, int* resident_rows, int* n_chunks,
+                             int64_t* resident_wb) {
   const int E = c->E;
   const int* hits = reinterpret_cast<const int*>(hinfo + 1);
   const uint8_t* pl = reinterpret_cast<const uint8_t*>(hits + E);
@@ -943,22 +991,28 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   const uint8_t* master = static_cast<const uint8_t*>(w->host_master);
   uint8_t* pool = static_cast<uint8_t*>(c->pool);
   const size_t xb = c->expert_bytes;
+  // the new slot maps are planned on copies and committed only after every enqueue succeeded
+  std::vector<int> slot_of = c->slot_of, owner = c->owner;
   std::vector<int> off(E), loaded0(E);
   for (int e = 0, r = 0; e < E; ++e) {  // same row rule as the FFN's build mode
     off[e] = r;
     r += hits[e];
-    loaded0[e] = c->slot_of[e] >= 0;
-    if (hits[e] > 0 && loaded0[e]) *weight_bytes += (int64_t)xb * ((hits[e] + kMaxTok - 1) / kMaxTok);
+    loaded0[e] = slot_of[e] >= 0;
+    if (hits[e] > 0 && loaded0[e]) {
+      *weight_bytes += (int64_t)xb * ((hits[e] + kMaxTok - 1) / kMaxTok);
+      *resident_rows += hits[e];
+    }
   }
+  *resident_wb = *weight_bytes;  // the resident launch: experts in HBM at step start
   std::vector<int> free_now, free_after_gemm1;
   for (int sl = 0; sl < C; ++sl)
-    if (c->owner[sl] < 0) free_now.push_back(sl);
+    if (owner[sl] < 0) free_now.push_back(sl);
   for (int e = 0; e < E; ++e) {
-    const int sl = c->slot_of[e];
+    const int sl = slot_of[e];
     if (sl >= 0 && !pl[e]) {
       (hits[e] > 0 ? free_after_gemm1 : free_now).push_back(sl);
-      c->owner[sl] = -1;
-      c->slot_of[e] = -1;
+      owner[sl] = -1;
+      slot_of[e] = -1;
     }
   }
   struct Copy { int e, dst; bool after_gemm1, staged; };
@@ -974,8 +1028,8 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
     Copy cp{e, -1, false, false};
     if (pl[e]) {
       cp.dst = take_slot(cp.after_gemm1);
-      c->owner[cp.dst] = e;
-      c->slot_of[e] = cp.dst;
+      owner[cp.dst] = e;
+      slot_of[e] = cp.dst;
     } else {
       cp.staged = true;
     }
@@ -983,11 +1037,11 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   }
   if (!lazy)
     for (int e = 0; e < E; ++e)
-      if (pl[e] && c->slot_of[e] < 0 && hits[e] == 0) {
+      if (pl[e] && slot_of[e] < 0 && hits[e] == 0) {
         Copy cp{e, -1, false, false};
         cp.dst = take_slot(cp.after_gemm1);
-        c->owner[cp.dst] = e;
-        c->slot_of[e] = cp.dst;
+        owner[cp.dst] = e;
+        slot_of[e] = cp.dst;
         cold_copies.push_back(cp);
       }
   *streamed = (int)hit_copies.size();
@@ -1005,6 +1059,7 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
     if (b < (int)hit_copies.size()) chunks.push_back({b, (int)hit_copies.size()});
   }
   if ((int)chunks.size() > c->max_chunks) return fail(TIDE_EINVAL, "too many staged chunks");
+  *n_chunks = (int)chunks.size();
   int ne = 0;
   std::vector<int> chunk_first(chunks.size() + 1, 0);
   for (size_t ci = 0; ci < chunks.size(); ++ci) {
@@ -1063,8 +1118,10 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   }
   CU_TRY(cudaEventRecord(c->ev_side_done, c->side));
   CU_TRY(cudaStreamWaitEvent(st, c->ev_side_done, 0));
-  for (int e = 0; e < E; ++e) c->h_slot_of[e] = c->slot_of[e];
+  for (int e = 0; e < E; ++e) c->h_slot_of[e] = slot_of[e];
   CU_TRY(cudaMemcpyAsync(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice, st));
+  c->slot_of = std::move(slot_of);
+  c->owner = std::move(owner);
   return TIDE_OK;
 }
 
@@ -1148,8 +1205,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
 
-  int streamed = 0, copies = 0;
-  int64_t weight_bytes = 0;
+  int streamed = 0, copies = 0, res_rows = 0, n_chunks = 0;
+  int64_t weight_bytes = 0, res_wb = 0;
   const RouteInfo* hinfo = nullptr;
   if (pool_mode) {  // ---------------- a6 + a8
     CU_TRY(cudaEventRecord(c->ev_gemm1, st));
@@ -1158,7 +1215,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     if (hinfo->status != 0)
       return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
                   step, capacity);
-    s = pool_step(c, w, hinfo, N, st, &streamed, &copies, &weight_bytes);
+    s = pool_step(c, w, hinfo, N, st, &streamed, &copies, &weight_bytes, &res_rows, &n_chunks,
+                  &res_wb);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
@@ -1211,8 +1269,17 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     } else {
       CU_TRY(cudaStreamSynchronize(st));
     }
-    if (shared) weight_bytes += (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok);
-    fill_stats(c, hinfo, N, streamed, copies, weight_bytes, stats);
+    const int64_t shared_wb = shared ? (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok) : 0;
+    weight_bytes += shared_wb;
+    if (!pool_mode) {  // one FFN launch computes everything
+      res_wb = weight_bytes;
+      res_rows = N * k;
+    } else {
+      res_wb += shared_wb;
+    }
+    if (shared) res_rows += N;
+    fill_stats(c, hinfo, N, streamed, copies, weight_bytes, stats, res_wb, res_rows,
+               (N > 0 ? 1 : 0) + n_chunks);
   }
   return TIDE_OK;
 }
@@ -1347,7 +1414,9 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     int64_t wb = 0;
     for (int e = 0; e < El; ++e) wb += (int64_t)c->expert_bytes * ((hl[e] + kMaxTok - 1) / kMaxTok);
     if (shared) wb += (int64_t)c->expert_bytes * ((N + kMaxTok - 1) / kMaxTok);
-    fill_stats(c, &local, N, 0, 0, wb, stats);
+    int pairs_l = 0;
+    for (int e = 0; e < El; ++e) pairs_l += hl[e];
+    fill_stats(c, &local, N, 0, 0, wb, stats, wb, pairs_l + (shared ? N : 0), 1);
     stats->nonresident_pairs = 0;
     for (int e = 0; e < El; ++e) stats->nonresident_pairs += hl[e];
     stats->nonresident_pairs -= local.resident_pairs;

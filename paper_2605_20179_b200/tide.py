@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libtide.so")
 
 TIDE_OK, TIDE_EINVAL, TIDE_ECAPACITY, TIDE_EPLACEMENT, TIDE_ECUDA, TIDE_ENCCL, TIDE_ENOMEM, \
     TIDE_EUNSUPPORTED = range(8)
+ABI_VERSION = 2  # include/tide.h TIDE_ABI_VERSION
 TIDE_F32, TIDE_BF16 = 0, 1
 TIDE_NORM_TOPK, TIDE_SHARED_EXPERT, TIDE_LAZY_PROMOTE = 1, 2, 4
 TIDE_COUNTER_WINDOW, TIDE_COUNTER_CUMULATIVE, TIDE_TIE_INCUMBENT = 8, 16, 32
@@ -56,7 +57,9 @@ class StepStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "refreshed", "resident_pairs", "nonresident_pairs", "promotions", "evictions",
         "unique_experts", "experts_streamed", "copies")] + [
-        ("h2d_bytes", ctypes.c_int64), ("weight_bytes_read", ctypes.c_int64)]
+        ("h2d_bytes", ctypes.c_int64), ("weight_bytes_read", ctypes.c_int64),
+        ("resident_weight_bytes", ctypes.c_int64), ("resident_rows", ctypes.c_int32),
+        ("ffn_launches", ctypes.c_int32)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -243,7 +246,9 @@ class Context:
                  debug: bool | str = False, stream=None) -> StepOutputs:
         """tide_moe_step.  Tensors: block_hidden [N,H] (device), router_w [E,H] (device),
         device_all [E, 3HF] device or host_master [E, 3HF] pinned host, shared_w [3HF]
-        device, placement [E] uint8 device."""
+        device, placement [E] uint8 device.  debug: True (routing outputs, logits and kernel
+        timestamps), "routing" (top-k, gates, pos, order, offsets only) or "trace"
+        (timestamps only); test instrumentation, returned in StepOutputs.debug."""
         d = self.desc
         N = block_hidden.shape[0]
         dev = block_hidden.device
@@ -276,6 +281,9 @@ class Context:
                          dtype=torch.int64, device=dev)}
             if debug == "trace":  # kernel timestamps only: no extra copies on the stream
                 dbg_t = {n: (v if n.endswith("_trace") else None) for n, v in dbg_t.items()}
+            elif debug == "routing":  # the routing outputs only (D2D copies, graph-capturable)
+                dbg_t = {n: (None if n.endswith("_trace") or n == "logits" else v)
+                         for n, v in dbg_t.items()}
             dbg = StepDebug(*((dbg_t[n].data_ptr() if dbg_t[n] is not None else None)
                               for n, _ in StepDebug._fields_))
         _check(lib().tide_moe_step(

@@ -49,11 +49,14 @@ class DeviceLayer:
 
 
 def near_tie_tokens(logits64: np.ndarray, k: int, gap=TIE_GAP) -> np.ndarray:
-    """R-17: flag tokens whose fp64 gaps among the top-(k+1) logits are < gap."""
+    """R-17: flag tokens whose fp64 gap between two adjacent logits among the top-(k+1) is
+    below `gap` but not zero.  An exact tie (gap 0) is not flagged: both sides then see equal
+    logits and the lowest-id rule (R-3) decides, so the selection must match exactly."""
     s = -np.sort(-logits64, axis=1)[:, : k + 1]
     if s.shape[1] < 2:
         return np.zeros(logits64.shape[0], bool)
-    return (np.abs(np.diff(s, axis=1)) < gap).any(axis=1)
+    d = np.abs(np.diff(s, axis=1))
+    return ((d < gap) & (d > 0)).any(axis=1)
 
 
 def rel_err(a, ref) -> float:

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_library_is_sm100a_only():
     tide = _lib()
-    assert tide.lib().tide_abi_version() == 1
+    assert tide.lib().tide_abi_version() == tide.ABI_VERSION
     assert tide.lib().tide_build_sm() == 100
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", tide.LIB_PATH],
@@ -101,3 +101,20 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(tide, "_lib", None)
     with pytest.raises(ImportError):
         tide.lib()
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors have the C structs' sizes (gcc on include/tide.h)."""
+    import ctypes
+    import subprocess
+    tide = _lib()
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "tide.h"\nint main(void){printf("%zu %zu %zu %zu %zu\\n",'
+                   'sizeof(tide_layer_desc), sizeof(tide_expert_weights), sizeof(tide_step_stats),'
+                   'sizeof(tide_step_debug), sizeof(tide_phase_times)); return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    want = [ctypes.sizeof(c) for c in (tide.LayerDesc, tide.ExpertWeights, tide.StepStats,
+                                       tide.StepDebug, tide.PhaseTimes)]
+    assert got == want

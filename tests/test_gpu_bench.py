@@ -41,8 +41,10 @@ def test_bench_single_process_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
-@pytest.mark.parametrize("extra", [[], ["--ep", "--p2p"]])
+@pytest.mark.parametrize("extra", [["--replicas"], []])
 def test_bench_torchrun_two_ranks_one_gpu(extra):
+    """torchrun x2 in the one-GPU test mode: replicas, and the N>1 default (flash-shaped
+    expert parallelism over peer memory, NVLink accounting) on a 2-layer stack."""
     env = dict(os.environ, TIDE_BENCH_SAME_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
@@ -51,4 +53,20 @@ def test_bench_torchrun_two_ranks_one_gpu(extra):
     assert r.returncode == 0, r.stderr[-2000:]
     d = _line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0
-    assert ("expert parallel x2" in d["config"]["parallelism"]) == bool(extra)
+    ep = not extra
+    assert ("expert parallel x2" in d["config"]["parallelism"]) == ep
+    if ep:
+        assert "flash" in d["config"]["workload"] and d["nvlink"]["bytes_out_per_layer_step"] > 0
+        assert 0 < d["roofline"]["frac"] < 1.2
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` (no torchrun) launches the two ranks itself."""
+    env = dict(os.environ, TIDE_BENCH_SAME_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--replicas", "--layers", "2", "--steps", "3",
+           "--warmup", "3", "--no-cpu", "--no-e2e"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _line(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0

@@ -74,29 +74,25 @@ def test_toy_schedule(mode):
 # ------------------------------------------------------------------ bf16 shapes
 @pytest.mark.parametrize("shape_name", ["mini", "flash"])
 def test_block_layer_parity(shape_name):
-    """BJ.configs[1]/[2] layer shapes, block of 32 tokens, C = E.  The oracle
-    computes the FFN for a sample of tokens (all routing is compared)."""
+    """BJ.configs[1]/[2] layer shapes, block of 32 tokens, C = E: every token's routing,
+    hits, placement, permutation and output against the oracle."""
     shape = g.SHAPES[shape_name]
     layer = DeviceLayer(shape, 11)
     ctx = _ctx(shape, shape.num_experts)
     x = g.block_hidden_np(shape, 11, steps=3)[2]
-    mask = np.zeros(shape.tokens, np.uint8)
-    mask[[0, 5, 17, 31]] = 1
     _run_and_check(shape, 11, x, layer, ctx, np.zeros(shape.num_experts, np.uint8), 0, 1,
-                   shape.num_experts, token_mask=mask)
+                   shape.num_experts)
 
 
 def test_sweep_batch_parity_capacity_limited():
     """BJ.configs[4]: mini shape, batch of 8 blocks (256 tokens), C = 64 with
-    pinned-host serving of non-resident experts; sampled outputs."""
+    pinned-host serving of non-resident experts; every token's output."""
     shape = g.SWEEP
     layer = DeviceLayer(shape, 12, host_master=True)
     ctx = _ctx(shape, 64)
     x = g.block_hidden_np(shape, 12, steps=1)[0]
-    mask = np.zeros(shape.tokens, np.uint8)
-    mask[[0, 100, 255]] = 1
     r, *_ = _run_and_check(shape, 12, x, layer, ctx, np.zeros(256, np.uint8), 0, 4, 64,
-                           mode="host_master", token_mask=mask)
+                           mode="host_master")
     assert r.stats["copies"] > 0 and r.stats["h2d_bytes"] == r.stats["copies"] * shape.expert_bytes
 
 
@@ -284,3 +280,24 @@ def test_many_experts_work_list_paths(E, H):
     ctx = _ctx(shape, E)
     x = g.block_hidden_np(shape, 19, steps=1)[0]
     _run_and_check(shape, 19, x, layer, ctx, np.zeros(E, np.uint8), 0, 1, E)
+
+
+def test_placement_over_capacity_device_all_leaves_placement_unchanged():
+    """tide.h: on TIDE_EPLACEMENT (non-refresh step, popcount(placement) > C) placement_out is
+    a copy of the input placement and hit_counts holds the step's hits (device_all mode
+    reports the status when stats are requested)."""
+    from paper_2605_20179_b200 import tide
+    layer = DeviceLayer(SMALL, 36)
+    ctx = _ctx(SMALL, 4, max_tokens=40)
+    x_np = g.block_hidden_np(SMALL, 36, steps=1)[0]
+    pin = torch.ones(12, dtype=torch.uint8, device="cuda")
+    pout = torch.full((12,), 7, dtype=torch.uint8, device="cuda")
+    hits = torch.full((12,), -1, dtype=torch.int32, device="cuda")
+    with pytest.raises(tide.TideError) as ei:
+        ctx.moe_step(g.np_to_torch(x_np, "cuda"), layer.router, **layer.weights(), placement=pin,
+                     step=1, interval=2, placement_out=pout, hit_counts=hits, stats=True)
+    assert ei.value.status == tide.TIDE_EPLACEMENT
+    torch.cuda.synchronize()
+    assert pout.cpu().numpy().tolist() == [1] * 12
+    ref = oracle.moe_step(layer.oracle_layer(), x_np, SMALL.top_k, np.zeros(12, np.uint8), 0, 1, 12)
+    assert (hits.cpu().numpy() == ref.hits).all()

@@ -292,20 +292,23 @@ def _uniform_torch_keys(keys, n: int, bound: float, device, out_dtype):
 
 
 def layer_torch(shape: Shape, seed: int, layer: int, device, chunk: int = 32,
-                skew: float = SKEW):
+                skew: float = SKEW, experts: range | None = None):
     """Device twin of layer_np: (wr [E,H], wg [E,F,H], wu [E,F,H], wd [E,H,F], shared|None),
-    bit-identical to the host generator, generated `chunk` experts at a time."""
+    bit-identical to the host generator, generated `chunk` experts at a time.  `experts`
+    (a contiguous id range, e.g. one EP rank's) restricts wg/wu/wd to those experts."""
     import torch
     dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
     E, H, F = shape.num_experts, shape.hidden, shape.ffn
-    wg = torch.empty(E, F, H, dtype=dt, device=device)
-    wu = torch.empty(E, F, H, dtype=dt, device=device)
-    wd = torch.empty(E, H, F, dtype=dt, device=device)
-    for e0 in range(0, E, chunk):
-        es = range(e0, min(E, e0 + chunk))
+    ids = range(E) if experts is None else experts
+    n_e = len(ids)
+    wg = torch.empty(n_e, F, H, dtype=dt, device=device)
+    wu = torch.empty(n_e, F, H, dtype=dt, device=device)
+    wd = torch.empty(n_e, H, F, dtype=dt, device=device)
+    for i0 in range(0, n_e, chunk):
+        es = ids[i0:i0 + chunk]
         for out, tag, n, fan in ((wg, T_WG, F * H, H), (wu, T_WU, F * H, H), (wd, T_WD, H * F, F)):
             keys = [_key(seed, layer, tag, e) for e in es]
-            out[e0:e0 + len(es)] = _uniform_torch_keys(keys, n, math.sqrt(3.0 / fan), device,
+            out[i0:i0 + len(es)] = _uniform_torch_keys(keys, n, math.sqrt(3.0 / fan), device,
                                                        dt).view(len(es), *out.shape[1:])
     shared = shared_torch(shape, seed, layer, device) if shape.shared_expert else None
     return router_torch(shape, seed, layer, device, skew=skew), wg, wu, wd, shared

@@ -4,7 +4,7 @@
       --print-units base --clock-control none -k regex:tide_ffn -c <L*T> --csv --log-file gpurun_out/ffn_<cfg>.csv \
       python tools/ffn_traffic.py --config mini --algo gpurun_out/ffn_<cfg>_algo.json
   python tools/ffn_traffic.py --config mini --join gpurun_out/ffn_<cfg>.csv \
-      --algo gpurun_out/ffn_<cfg>_algo.json            # -> profiles/ffn_traffic.json[cfg]
+      --algo gpurun_out/ffn_<cfg>_algo.json  # -> profiles/ffn_traffic.json["<cfg>|calibrated|C=256|ep=none|L=<layers>"]
 
 The run pushes exactly one block (t = 0..T-1) through the whole stack in bench.py's order
 (layer-major within a step, C = E, interval 4). The first L*T FFN launches are the ones
@@ -56,7 +56,10 @@ if a.join:
                     f"(tools/ffn_traffic.py)")}
     out = os.path.join(ROOT, "profiles", "ffn_traffic.json")
     allr = json.load(open(out)) if os.path.exists(out) else {}
-    allr[a.config] = res
+    key = f"{a.config}|calibrated|C=256|ep=none|L={algo['layers']}"  # bench.py's lookup key
+    res["config"] = {"shape": a.config, "routing": "calibrated", "capacity": 256, "ep": "none",
+                     "layers": algo["layers"]}
+    allr[key] = res
     json.dump(allr, open(out, "w"), indent=1)
     print(json.dumps(res))
     sys.exit(0)
