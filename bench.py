@@ -922,6 +922,9 @@ def run_reference(args, world: int):
                     "d2h_bytes_per_step": 0}}
 
 
+_OUT = sys.stdout
+
+
 def _free_port() -> int:
     so = socket.socket()
     so.bind(("127.0.0.1", 0))
@@ -940,11 +943,18 @@ def spawn(args) -> int:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
            str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    return subprocess.call(cmd, stdout=_OUT)
 
 
 def main():
     args = parse()
+    # stdout carries the one JSON line: anything native code prints (NCCL's version banner,
+    # init lines) goes to stderr, the line itself to the saved stdout
+    sys.stdout.flush()
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    global _OUT
+    _OUT = os.fdopen(out_fd, "w")
     world_env = os.environ.get("WORLD_SIZE")
     if world_env is None and args.gpus > 1:
         sys.exit(spawn(args))
@@ -956,13 +966,14 @@ def main():
         sys.exit(2)
     if args.impl == "reference":  # the oracle has no multi-GPU form: rank 0 alone
         if rank == 0:
-            print(json.dumps(run_reference(args, world)), flush=True)
+            print(json.dumps(run_reference(args, world)), file=_OUT, flush=True)
         return
     # test mode for the multi-process code path on a one-GPU box: every rank on cuda:0 and a
     # gloo process group (NCCL refuses two ranks per device); replicas and peer-memory EP only
     same_dev = bool(os.environ.get("TIDE_BENCH_SAME_DEVICE"))
     if same_dev:
         local_rank = 0
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the JSON line only
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # keep the NCCL init lines (comm size)
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -973,7 +984,7 @@ def main():
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_tide(args, rank, world, local_rank, nccl_ok=not (same_dev and world > 1))
     if rank == 0:
-        print(json.dumps(res), flush=True)
+        print(json.dumps(res), file=_OUT, flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 

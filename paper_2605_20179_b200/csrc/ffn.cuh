@@ -506,11 +506,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if constexpr (EP) {  // every CTA fences its own peer y stores at system scope, then arrives
+  if constexpr (EP) {  // every CTA releases its own peer y stores at system scope as it arrives
     __shared__ int s_last;
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      s_last = atomicAdd(p.ep_done, 1) == (int)gridDim.x - 1;
+      s_last = (p.ep_P > 1 ? atom_add_acq_rel_sys(p.ep_done, 1) : atom_add_acq_rel_gpu(p.ep_done, 1)) ==
+               (int)gridDim.x - 1;
     }
     __syncthreads();
     if (s_last) {  // the grid's last CTA: counts to every rank, one system fence, arrive

@@ -76,6 +76,14 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// The same arrival at system scope: used by CTAs that stored into a peer GPU's memory, so
+// their own release (MEMBAR.ALL.SYS, no sequentially-consistent fence) covers those stores
+// before anyone downstream can observe the arrival.
+__device__ __forceinline__ int atom_add_acq_rel_sys(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.sys.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }

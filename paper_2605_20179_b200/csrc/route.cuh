@@ -253,12 +253,13 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   __syncthreads();
   if (tid == 0) {
     if (tr) tr[1] = globaltimer_ns();
-    // EP: this CTA's peer stores (X slices) are made visible at system scope by the CTA
-    // itself (after the barrier, cumulative over the CTA's threads), not only through the
-    // gpu-scope arrival chain to the grid's last CTA
-    if (p.ep_P) __threadfence_system();
-    // release this CTA's logits; acquire the earlier arrivals' for the group's phase 2
-    s_flag = atom_add_acq_rel_gpu(&p.g_cnt[blockIdx.y], 1) == (int)gridDim.x - 1;
+    // release this CTA's logits; acquire the earlier arrivals' for the group's phase 2.
+    // EP: the release is at system scope, so this CTA's own peer stores (X slices) are
+    // published by the CTA itself (after the barrier, cumulative over its threads), not
+    // only through the gpu-scope arrival chain to the grid's last CTA
+    const int old = p.ep_P > 1 ? atom_add_acq_rel_sys(&p.g_cnt[blockIdx.y], 1)
+                           : atom_add_acq_rel_gpu(&p.g_cnt[blockIdx.y], 1);
+    s_flag = old == (int)gridDim.x - 1;
   }
   __syncthreads();
   if (!s_flag) return;
@@ -292,8 +293,9 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
-    if (p.ep_P) __threadfence_system();  // this CTA's peer top-k / gate stores (see above)
-    if (atom_add_acq_rel_gpu(p.g_done, 1) == (int)gridDim.y - 1) {  // every CTA has read par
+    // every CTA has read par; EP: system-scope release of this CTA's peer top-k / gate stores
+    const int old = p.ep_P > 1 ? atom_add_acq_rel_sys(p.g_done, 1) : atom_add_acq_rel_gpu(p.g_done, 1);
+    if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
       if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
