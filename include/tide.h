@@ -144,8 +144,10 @@ typedef struct {
   int32_t* order;    /* [E] expert at each bucket position                        */
   int32_t* offsets;  /* [E + 1] first row of each bucket position                 */
   float* logits;     /* [N, E] fp32 router logits                                 */
-  uint64_t* route_trace; /* [4 * route CTAs] %globaltimer ns per route-kernel CTA:
-                            start, phase 1 done, phase 2 start, phase 2 done (0 = n/a) */
+  uint64_t* route_trace; /* [8 * route CTAs] %globaltimer ns per route-kernel CTA:
+                            start, phase 1 done, phase 2 start, phase 2 done, then (phase-2
+                            CTAs, warp 0) logits loaded, selection done, histogram done
+                            (0 = n/a); needs >= 8 * ceil(E/8) * ceil(N/4) entries       */
   uint64_t* ffn_trace;   /* [8 * #SMs] per FFN CTA: entry, work list ready, producer done,
                             epilogue done (%globaltimer ns), items processed                */
   uint64_t* ffn_item_trace; /* [4 * 64 * #SMs] per FFN CTA, its first 64 items: claim time,

@@ -80,13 +80,12 @@ struct RouteParams {
                         // into cnt2[par] (zero on entry) and zeroes cnt2[par^1] for the next
   int* par;             // device parity word, flipped by the last CTA (so any stream-ordered
                         // or graph-replayed sequence of steps stays consistent)
-  int* g_done;          // completion counter of the phase-2 CTAs (self-resetting)
-  int* list;            // [E * maxN] tokens of each expert (arrival order)
+  int* g_done;          // completion counter of the phase-2 CTAs (self-resetting)  int* list;            // [E * maxN] tokens of each expert (arrival order)
   unsigned* mask;       // [E * NW] token bitmasks (zeroed by tide_book_kernel)
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
   int n_zero;
-  unsigned long long* trace;  // debug: 4 timestamps per CTA (nullable)
+  unsigned long long* trace;  // debug: 8 timestamps per CTA (nullable)
   // Peer-memory EP dispatch fused into the router (tide_ctx_create_ep_p2p; ep_P == 0: off).
   // Every CTA stores its slice of its token rows of X into every rank's x_all; each token
   // group's phase-2 CTA stores the group's top-k ids and gates; the grid's last CTA stores
@@ -122,6 +121,10 @@ struct BookParams {
 
 __device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
   return va > vb || (va == vb && ia < ib);
+}
+// The same order without short-circuit evaluation (predicate logic, no branches).
+__device__ __forceinline__ bool better_nb(float va, int ia, float vb, int ib) {
+  return (va > vb) | ((va == vb) & (ia < ib));
 }
 // Order-preserving uint32 key of a float (-0 folded into +0, so key order == float order,
 // equal floats <=> equal keys): the warp argmax below runs on redux.sync.
@@ -177,7 +180,8 @@ __device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 
 // lists and bitmasks by atomics.
 template <int EPL>
 __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int n,
-                                            const float (&v_in)[EPL]) {
+                                            const float (&v_in)[EPL],
+                                            unsigned long long* tr = nullptr) {
   const int lane = threadIdx.x & 31;
   const int E = p.E, k = p.k, NW = (p.N + 31) >> 5;
   {
@@ -189,13 +193,25 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
       v[i] = e < E ? v_in[i] : -INFINITY;
       id[i] = e;
     }
+    // bitonic sorting network over the lane's EPL logits (compile-time indices, branch-free
+    // compare-exchanges: the previous bubble sort compiled to one branch per comparison)
 #pragma unroll
-    for (int a = 0; a < EPL; ++a)
+    for (int kk = 2; kk <= EPL; kk <<= 1)
 #pragma unroll
-      for (int b = 0; b + 1 < EPL - a; ++b)
-        if (better(v[b + 1], id[b + 1], v[b], id[b])) {
-          const float tv = v[b]; v[b] = v[b + 1]; v[b + 1] = tv;
-          const int ti = id[b]; id[b] = id[b + 1]; id[b + 1] = ti;
+      for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const int l = i ^ jj;
+          if (l > i) {  // compile-time
+            const int a = (i & kk) == 0 ? i : l, b = (i & kk) == 0 ? l : i;  // a ranks first
+            const bool sw = better_nb(v[b], id[b], v[a], id[a]);
+            const float va = v[a], vb = v[b];
+            const int ia = id[a], ib = id[b];
+            v[a] = sw ? vb : va;
+            v[b] = sw ? va : vb;
+            id[a] = sw ? ib : ia;
+            id[b] = sw ? ia : ib;
+          }
         }
     float m = v[0];  // row max
 #pragma unroll
@@ -230,6 +246,10 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
 #pragma unroll
       for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       denom = t;
+    }
+    if (tr && lane == 0) {  // debug: selection and gates done (after a use of denom)
+      if (denom == 1.2345e-30f) tr[7] = 2;
+      tr[5] = globaltimer_ns();
     }
     if (lane < k) {
       p.topk_idx[(size_t)n * k + lane] = my_e;
@@ -278,8 +298,16 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
       const int e = lane + 32 * i;
       v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
     }
-    route_token<EPL>(p, cnt, n, v);
+    if (tr && n == n0) {  // debug: logits arrived (in-order issue after a use of every value)
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) s += v[i];
+      if (s == 1.2345e-30f) tr[7] = 1;
+      if (lane == 0) tr[4] = globaltimer_ns();
+    }
+    route_token<EPL>(p, cnt, n, v, (tr && n == n0) ? tr : nullptr);
   }
+  if (tr && tid == 0) tr[6] = globaltimer_ns();
   __syncthreads();
   if (p.ep_P) {  // dispatch this group's routing to every rank
     const int k = p.k, rows = n1 - n0, tot = p.ep_P * rows * k;
@@ -297,8 +325,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     const int old = p.ep_P > 1 ? atom_add_acq_rel_sys(p.g_done, 1) : atom_add_acq_rel_gpu(p.g_done, 1);
     if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
-      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
-      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
+      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
                      // g_cnt / g_done chains; one system-scope fence publishes them: arrive
         for (int dst = 0; dst < p.ep_P; ++dst)
           reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
@@ -340,8 +367,8 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   pdl_wait();     // X may be written by the previous kernel in the stream
   pdl_trigger();  // let the FFN grid start its prologue
   unsigned long long* tr =
-      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
+      p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }
   const int par = __ldcg(p.par);  // read before this CTA arrives: the flip comes after all arrive
   int* cnt = p.cnt2 + par * E;
   if (blockIdx.x == 0 && blockIdx.y == 0) {
@@ -427,8 +454,8 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   pdl_wait();
   pdl_trigger();
   unsigned long long* tr =
-      p.trace ? p.trace + 4 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = 0; }
+      p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }
   const int par = __ldcg(p.par);
   int* cnt = p.cnt2 + par * E;
   if (blockIdx.x == 0 && blockIdx.y == 0) {

@@ -423,7 +423,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->gates, sizeof(float) * N * k);
   ALLOC(c->pair_slot, sizeof(int) * N * k);
   ALLOC(c->cnt, sizeof(int) * 2 * E);
-  ALLOC(c->cnt_par, sizeof(int) * 2);
+  ALLOC(c->cnt_par, sizeof(int) * 2);  // parity word, route completion counter
   ALLOC(c->pf_list, sizeof(int) * E);
   ALLOC(c->pf_n, sizeof(int));
   ALLOC(c->list, sizeof(int) * (size_t)E * N);

@@ -24,7 +24,7 @@ for t in range(8):
     r = ctx.moe_step(xs[t], wr, device_all=packed, shared_w=shared, placement=pl, step=t,
                      interval=4, debug=True)
 torch.cuda.synchronize()
-tr = r.debug["route_trace"].cpu().numpy().reshape(-1, 4).astype(np.int64)
+tr = r.debug["route_trace"].cpu().numpy().reshape(-1, 8).astype(np.int64)
 tpc = 4 if N <= 64 else 8
 ny = max(1, (N + tpc - 1) // tpc)
 tr = tr[: ((E + 7) // 8) * ny]

@@ -37,7 +37,7 @@ tpc = int(os.environ.get("TIDE_ROUTE_TPC", 4 if N <= 64 else 8))
 ny = max(1, (N + tpc - 1) // tpc)
 rows = []
 for li, r in enumerate(res):
-    rt = r.debug["route_trace"].cpu().numpy().reshape(-1, 4).astype(np.int64)
+    rt = r.debug["route_trace"].cpu().numpy().reshape(-1, 8).astype(np.int64)
     rt = rt[rt[:, 0] > 0]
     ft = r.debug["ffn_trace"].cpu().numpy().reshape(-1, 8).astype(np.int64)
     ft = ft[ft[:, 0] > 0]
@@ -46,7 +46,9 @@ for li, r in enumerate(res):
                      f0=ft[:, 0].min(), fl=ft[:, 1].min(), flx=ft[:, 1].max(), fp=ft[:, 2].max(),
                      fe=ft[:, 3].max(), fe_med=np.median(ft[:, 3]), fw=ft[:, 5].min(),
                      fwx=ft[:, 5].max(), r0x=rt[:, 0].max(), c0=ft[0, 6], c1=ft[0, 7],
-                     p1med=np.median(rt[:, 1] - rt[:, 0]), p2med=np.median(last[:, 3] - last[:, 2])))
+                     p1med=np.median(rt[:, 1] - rt[:, 0]), p2med=np.median(last[:, 3] - last[:, 2]),
+                     p2_load=np.median(last[:, 4] - last[:, 2]), p2_sel=np.median(last[:, 5] - last[:, 4]),
+                     p2_atom=np.median(last[:, 6] - last[:, 5]), p2_sync=np.median(last[:, 3] - last[:, 6])))
 t0 = rows[1]["r0"]
 us = lambda v: (v - t0) / 1e3  # noqa: E731
 print(f"{shape.name} t={T_AT}: times in us relative to layer 1's route start")
@@ -57,7 +59,9 @@ for li in range(1, NL):
           f"epi med {us(R['fe_med']):7.2f} max {us(R['fe']):7.2f}")
     print(f"   combine start (latest) {us(R['c0']):7.2f} end (latest) {us(R['c1']):7.2f}")
     print(f"   route CTA start spread {(R['r0x'] - R['r0']) / 1e3:5.2f}  per-CTA phase1 median {R['p1med'] / 1e3:5.2f}"
-          f"  phase2 median {R['p2med'] / 1e3:5.2f}")
+          f"  phase2 median {R['p2med'] / 1e3:5.2f} = logits {R['p2_load'] / 1e3:5.2f} + select "
+          f"{R['p2_sel'] / 1e3:5.2f} + histogram atomics {R['p2_atom'] / 1e3:5.2f} + barrier "
+          f"{R['p2_sync'] / 1e3:5.2f}")
     if li + 1 < NL:
         print(f"   gap ffn end -> next route start {us(rows[li + 1]['r0']) - us(R['fe']):6.2f} us "
               f"(combine + launch)")
