@@ -48,7 +48,8 @@ struct FfnParams {
   // experts in id order with m > 0 and (slot_of == nullptr or slot_of[e] >= 0), rows
   // off[e] = prefix of counts in id order, then the shared expert (rows N*k + n).
   const int* cnt;        // [E] per-expert token counts (build mode), or [2][E] with par
-  const int* par;        // nullable: route's parity word, this step's counts = cnt[par^1]  // NEXT-3 prefetch of the next layer (pf_base == nullptr: off)
+  const int* par;        // nullable: route's parity word, this step's counts = cnt[par^1]
+  // NEXT-3 prefetch of the next layer (pf_base == nullptr: off)
   const uint8_t* pf_base;  // next layer's packed experts (device_all)
   const int* pf_list;      // next layer's experts ranked by hits at its previous step
   const int* pf_n;         // number of ranked (hit) experts
@@ -504,7 +505,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
-  }  if constexpr (EP) {  // every CTA releases its own peer y stores at system scope as it arrives
+  }
+  if constexpr (EP) {  // every CTA releases its own peer y stores at system scope as it arrives
     __shared__ int s_last;
     if (threadIdx.x == 0) {
       s_last = (p.ep_P > 1 ? atom_add_acq_rel_sys(p.ep_done, 1) : atom_add_acq_rel_gpu(p.ep_done, 1)) ==

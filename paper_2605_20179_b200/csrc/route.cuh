@@ -80,7 +80,8 @@ struct RouteParams {
                         // into cnt2[par] (zero on entry) and zeroes cnt2[par^1] for the next
   int* par;             // device parity word, flipped by the last CTA (so any stream-ordered
                         // or graph-replayed sequence of steps stays consistent)
-  int* g_done;          // completion counter of the phase-2 CTAs (self-resetting)  int* list;            // [E * maxN] tokens of each expert (arrival order)
+  int* g_done;          // completion counter of the phase-2 CTAs (self-resetting)
+  int* list;            // [E * maxN] tokens of each expert (arrival order)
   unsigned* mask;       // [E * NW] token bitmasks (zeroed by tide_book_kernel)
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
@@ -325,7 +326,8 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     const int old = p.ep_P > 1 ? atom_add_acq_rel_sys(p.g_done, 1) : atom_add_acq_rel_gpu(p.g_done, 1);
     if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
-      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
+      *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
+      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
                      // g_cnt / g_done chains; one system-scope fence publishes them: arrive
         for (int dst = 0; dst < p.ep_P; ++dst)
           reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
