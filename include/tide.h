@@ -337,6 +337,34 @@ TIDE_API tide_status tide_interval_cost(const tide_interval_model* m, int32_t ta
 TIDE_API tide_status tide_optimize_interval(const tide_interval_model* m, int32_t* tau_out,
                                             double* curve);
 
+/* NEXT-2 on B200 (DESIGN R-21): the same trade-off (Eq. 5 migrations vs Eq. 6 misses,
+ * Eq. 7 scan) with the expert counts measured on a routing trace instead of derived from
+ * a constant drift, and with the experts that stream at every step (hit but outside even
+ * a fresh placement: R-13) included.  From host per-step hit counts [T][E]:
+ *   miss_lag[j] = mean over t of |{e : counts[t+j][e] > 0} \ topB(counts[t])|
+ *                 (hit experts outside a placement refreshed j steps earlier: streamed)
+ *   mig_lag[j]  = mean over t of |topB(counts[t+j]) \ topB(counts[t])|
+ *                 (promotions when a j-step-old placement is refreshed; Eq. 4 at lag j, x B)
+ * for j = 0..T-1, means over t = 0..T-1-j; topB = the placement rule (hits desc, id asc,
+ * R-8).  miss_lag / mig_lag: host [T].  1 <= B <= E, T >= 1.                            */
+TIDE_API tide_status tide_interval_profile(const int32_t* counts, int32_t T, int32_t E, int32_t B,
+                                           double* miss_lag, double* mig_lag);
+/* Expert copies over a block of T steps when refreshing every tau steps (1 <= tau < T):
+ *   copies(tau) = (T / tau) * (mig_lag[tau] + sum_{j < tau} miss_lag[j])
+ * cost = c_io * copies + T * c_step (c_io: seconds per expert H2D copy; c_step: the
+ * step's time without expert I/O).  tau* = argmin over [1, T-1], ties -> smallest tau;
+ * curve: host [T-1] costs or NULL.                                                       */
+typedef struct {
+  int32_t T;
+  double c_io, c_step;
+  const double* miss_lag;  /* host [T] from tide_interval_profile */
+  const double* mig_lag;   /* host [T] */
+} tide_interval_trace_model;
+TIDE_API tide_status tide_interval_cost_trace(const tide_interval_trace_model* m, int32_t tau,
+                                              double* copies, double* cost);
+TIDE_API tide_status tide_optimize_interval_trace(const tide_interval_trace_model* m,
+                                                  int32_t* tau_out, double* curve);
+
 /* NEXT-4: routing-trace analytics on the device.
  *  counts : device [T][E] int32 per-step hit counts (e.g. hit_counts of T steps)
  *  sim    : device [T][T] fp64 cosine similarity of the count vectors (0 if a vector is 0)

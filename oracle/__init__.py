@@ -361,3 +361,21 @@ def placement_ex(key, capacity, refresh, incumbent_ties, placement_in):
     assert lib().orc_placement_ex(k_.shape[0], capacity, _p(k_), int(refresh), int(incumbent_ties),
                                   _p(pin), _p(out)) == 0
     return out
+
+
+def interval_profile(counts, B):
+    """NEXT-2 on B200: (miss_lag [T], mig_lag [T]) of a [T, E] hit-count trace."""
+    c = np.ascontiguousarray(counts, np.int32)
+    T, E = c.shape
+    miss = np.empty(T, np.float64)
+    mig = np.empty(T, np.float64)
+    assert lib().orc_interval_profile(T, E, B, _p(c), _p(miss), _p(mig)) == 0
+    return miss, mig
+
+
+def interval_copies_trace(T, tau, miss_lag, mig_lag):
+    f = _d("orc_interval_copies_trace")
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    a = np.ascontiguousarray(miss_lag, np.float64)
+    b = np.ascontiguousarray(mig_lag, np.float64)
+    return f(T, tau, _p(a), _p(b))

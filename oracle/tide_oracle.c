@@ -483,3 +483,36 @@ int orc_placement_ex(int E, int capacity, const int32_t* key, int refresh, int i
   }
   return 0;
 }
+
+/* ---------------- NEXT-2 on B200 (DESIGN R-21): the interval trade-off on a routing trace --
+ * miss_lag[j] = mean over t of |{e : counts[t+j][e] > 0} \ topB(counts[t])| (hit experts
+ * outside a placement refreshed j steps earlier, streamed per R-13), mig_lag[j] = mean over t
+ * of |topB(counts[t+j]) \ topB(counts[t])| (promotions at a refresh of a j-step-old
+ * placement: Eq. 4's drift at lag j, times B), t = 0..T-1-j; topB is O6's rule.          */
+int orc_interval_profile(int T, int E, int B, const int32_t* counts, double* miss_lag,
+                         double* mig_lag) {
+  if (T < 1 || E < 1 || B < 1 || B > E) return 1;
+  uint8_t* top = (uint8_t*)malloc((size_t)T * E);
+  for (int t = 0; t < T; ++t)
+    orc_placement(E, B, counts + (size_t)t * E, 1, top + (size_t)t * E, top + (size_t)t * E);
+  for (int j = 0; j < T; ++j) {
+    long miss = 0, mig = 0;
+    for (int t = 0; t + j < T; ++t)
+      for (int e = 0; e < E; ++e) {
+        if (counts[(size_t)(t + j) * E + e] > 0 && !top[(size_t)t * E + e]) miss++;
+        if (top[(size_t)(t + j) * E + e] && !top[(size_t)t * E + e]) mig++;
+      }
+    miss_lag[j] = (double)miss / (double)(T - j);
+    mig_lag[j] = (double)mig / (double)(T - j);
+  }
+  free(top);
+  return 0;
+}
+
+/* Copies over a block of T steps refreshing every tau steps: T/tau intervals, each one
+ * refresh (mig_lag[tau] promotions) and tau steps of misses (miss_lag[0..tau-1]).        */
+double orc_interval_copies_trace(int T, int tau, const double* miss_lag, const double* mig_lag) {
+  double per = mig_lag[tau];
+  for (int j = 0; j < tau; ++j) per += miss_lag[j];
+  return (double)T / (double)tau * per;
+}

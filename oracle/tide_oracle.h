@@ -148,6 +148,11 @@ int orc_unique(int E, const int32_t* hits);
 /* Eq. 4: d = |topB(cur) \ topB(prev)| / B, top-B by (hits desc, id asc).           */
 double orc_drift(int E, int B, const int32_t* prev, const int32_t* cur);
 
+/* NEXT-2 on B200 (DESIGN R-21): interval trade-off measured on a routing trace [T][E]. */
+int orc_interval_profile(int T, int E, int B, const int32_t* counts, double* miss_lag,
+                         double* mig_lag);
+double orc_interval_copies_trace(int T, int tau, const double* miss_lag, const double* mig_lag);
+
 #ifdef __cplusplus
 }
 #endif

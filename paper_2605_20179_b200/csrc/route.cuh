@@ -72,6 +72,8 @@ struct RouteParams {
   const void* wr;       // [E,H] router
   void* x_in;           // [maxN,H] context copy of X (FFN gather source)
   float* logits;        // [N,E]
+  double* logits64;     // [ksplit][maxN][E] fp64 partials over slices of H (TC router, ksplit > 1)
+  int ksplit;           // TC router: CTAs per 16-expert tile, each over H / ksplit (1 or 2)
   int N, E, H, k, tpc, norm_topk, maxN;
   int* topk_idx;        // [N,k]
   float* gates;         // [N,k]
@@ -86,6 +88,8 @@ struct RouteParams {
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
   int n_zero;
+  int* zero_c;          // fused-combine counters zeroed by the whole grid
+  int n_zero_c;
   unsigned long long* trace;  // debug: 8 timestamps per CTA (nullable)
   // Peer-memory EP dispatch fused into the router (tide_ctx_create_ep_p2p; ep_P == 0: off).
   // Every CTA stores its slice of its token rows of X into every rank's x_all; each token
@@ -294,10 +298,31 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
   // registers, then k rounds of a warp argmax over the lanes' heads; the winner pops.
   for (int n = n0 + warp; n < n1; n += kRouteThreads / 32) {
     float v[EPL];
+    if (p.ksplit > 1) {  // sum the fp64 slices in slice order, round once (R-17)
+      double s[EPL];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
-      const int e = lane + 32 * i;
-      v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+      for (int i = 0; i < EPL; ++i) {
+        const int e = lane + 32 * i;
+        s[i] = e < E ? __ldcg(p.logits64 + (size_t)n * E + e) : 0.0;
+      }
+      for (int q = 1; q < p.ksplit; ++q)
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const int e = lane + 32 * i;
+          if (e < E) s[i] += __ldcg(p.logits64 + ((size_t)q * p.maxN + n) * E + e);
+        }
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int e = lane + 32 * i;
+        v[i] = e < E ? (float)s[i] : -INFINITY;
+        if (e < E) p.logits[(size_t)n * E + e] = v[i];  // the fp32 logits (debug output)
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int e = lane + 32 * i;
+        v[i] = e < E ? __ldcg(p.logits + (size_t)n * E + e) : -INFINITY;
+      }
     }
     if (tr && n == n0) {  // debug: logits arrived (in-order issue after a use of every value)
       float s = 0.f;
@@ -378,6 +403,10 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
     for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
   }
+  {  // the fused combine's (token, H-tile) counters, spread over the grid
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
+    for (int i = cta * blockDim.x + tid; i < p.n_zero_c; i += ncta * blockDim.x) p.zero_c[i] = 0;
+  }
 
   // ================= phase 1: router logits (a1)
   {
@@ -452,7 +481,8 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   __shared__ double s_red[kRouteThreads / 32][32][4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int E = p.E, N = p.N, H = p.H;
-  const int n0 = blockIdx.y * 8, n1 = min(N, n0 + 8), e0 = blockIdx.x * 16;
+  const int S = p.ksplit, ks = blockIdx.x % S;  // this CTA's slice of H (S slices per tile)
+  const int n0 = blockIdx.y * 8, n1 = min(N, n0 + 8), e0 = (blockIdx.x / S) * 16;
   pdl_wait();
   pdl_trigger();
   unsigned long long* tr =
@@ -465,6 +495,10 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
     for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
   }
+  {  // the fused combine's (token, H-tile) counters, spread over the grid
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
+    for (int i = cta * blockDim.x + tid; i < p.n_zero_c; i += ncta * blockDim.x) p.zero_c[i] = 0;
+  }
   // ================= phase 1: router logits (a1)
   {
     const int g = lane >> 2, c = lane & 3;
@@ -473,7 +507,8 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
     const uint4* wb = reinterpret_cast<const uint4*>(wr + (size_t)(e0 + g + 8) * H);
     const uint4* xt = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.x) +
                                                      (size_t)max(0, min(n0 + g, N - 1)) * H);
-    const int kw = H / (kRouteThreads / 32), kbeg = warp * kw;  // this warp's k range
+    // this warp's k range: slice ks of H, split over the 8 warps
+    const int kw = H / (S * (kRouteThreads / 32)), kbeg = ks * (H / S) + warp * kw;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int kb = kbeg; kb < kbeg + kw; kb += 32 * G) {
       uint4 A0[G], A1[G], B[G];
@@ -521,7 +556,12 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
       double v = 0.0;
 #pragma unroll
       for (int w = 0; w < kRouteThreads / 32; ++w) v += s_red[w][ln][rg];
-      if (n0 + q < N) p.logits[(size_t)(n0 + q) * E + e0 + r] = (float)v;
+      if (n0 + q < N) {
+        if (S == 1)
+          p.logits[(size_t)(n0 + q) * E + e0 + r] = (float)v;
+        else  // fp64 partial of this K slice; phase 2 sums the S slices in order
+          p.logits64[((size_t)ks * p.maxN + n0 + q) * E + e0 + r] = v;
+      }
     }
   }
   route_ep_push_x<__nv_bfloat16>(p, n0, n1);

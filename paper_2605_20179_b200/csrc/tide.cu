@@ -138,6 +138,15 @@ struct tide_ctx {
   void* x_in = nullptr;      // [maxN, H] copy of the block's hidden states (gather4 source)
   void* h_perm = nullptr;    // [max_rows, F]
   float* y_perm = nullptr;   // [max_rows, H]
+  int* cmb_cnt = nullptr;    // [maxN * ceil(H/128)] fused-combine arrival counters
+  // A/B measurement knobs, read once from the environment at context creation:
+  // TIDE_ROUTE_TPC (tokens per CUDA-core router CTA), TIDE_ROUTER_CC=1 (CUDA-core router for
+  // bf16), TIDE_ROUTE_ONE_PER_SM=1 (one router CTA per SM), TIDE_FUSED_COMBINE=1 (a10 in
+  // the FFN's phase-2 epilogue instead of the combine kernel: experimental, DESIGN 11)
+  int knob_route_tpc = 0;
+  bool knob_router_cc = false, knob_route_one_per_sm = false, knob_fused_combine = false;
+  bool knob_route_ksplit1 = false;  // TIDE_ROUTE_KSPLIT1=1: one router CTA per 16 x 8 tile
+  double* logits64 = nullptr;       // [2][maxN][E] fp64 router partials (bf16, TC router)
   int* ffn_ctrl = nullptr;   // [2 + max_entries]: scheduler counter, per-entry done counters,
                              // grid arrival counter (peer-memory EP)
   RouteInfo* info = nullptr; // + hits[E] + placement[E]
@@ -348,7 +357,8 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n,
+                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n, c->cmb_cnt,
+                 c->logits64,
                  c->dst_l};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -419,6 +429,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->max_entries = E / world + (world * N * k) / kMaxTok + 2 + (N + kMaxTok - 1) / kMaxTok;
 
   ALLOC(c->logits, sizeof(float) * N * E);
+  if (c->bf16) ALLOC(c->logits64, sizeof(double) * 2 * N * E);  // TC router's H-split partials
   ALLOC(c->topk, sizeof(int) * N * k);
   ALLOC(c->gates, sizeof(float) * N * k);
   ALLOC(c->pair_slot, sizeof(int) * N * k);
@@ -437,6 +448,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->h_perm, c->eb * (size_t)c->max_rows * c->F);
   ALLOC(c->y_perm, sizeof(float) * (size_t)c->max_rows * c->H);
   ALLOC(c->ffn_ctrl, sizeof(int) * (2 + c->max_entries));
+  ALLOC(c->cmb_cnt, sizeof(int) * (size_t)N * ((c->H + kTileM - 1) / kTileM));
   c->info_bytes = sizeof(RouteInfo) + sizeof(int) * E + E;
   ALLOC(c->info, c->info_bytes);
   ALLOC(c->slot_of_dev, sizeof(int) * E);
@@ -475,6 +487,11 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
     return fail(TIDE_ECUDA, "ctx init: %s", cudaGetErrorString(e));
   }
   c->slot_of.assign(E, -1);
+  if (const char* v = getenv("TIDE_ROUTE_TPC")) c->knob_route_tpc = std::max(1, std::min(8, atoi(v)));
+  c->knob_router_cc = getenv("TIDE_ROUTER_CC") != nullptr;
+  c->knob_route_one_per_sm = getenv("TIDE_ROUTE_ONE_PER_SM") != nullptr;
+  c->knob_fused_combine = getenv("TIDE_FUSED_COMBINE") != nullptr;
+  c->knob_route_ksplit1 = getenv("TIDE_ROUTE_KSPLIT1") != nullptr;
   *out = c;
   return TIDE_OK;
 }
@@ -716,7 +733,8 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
                               int N, cudaStream_t st, bool ep_local = false,
                               unsigned long long* trace = nullptr, const int* par = nullptr,
-                              bool prefetch = false, unsigned long long* itrace = nullptr) {
+                              bool prefetch = false, unsigned long long* itrace = nullptr,
+                              void* cmb_out = nullptr) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -780,6 +798,11 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   }
   p.shared_row0 = N * c->k;
   p.shared_tok0 = 0;
+  p.cmb_out = (cmb_out && !ep_local) ? cmb_out : nullptr;  // a10 in the phase-2 epilogue
+  p.cmb_cnt = c->cmb_cnt;
+  p.cmb_topk = c->topk;
+  p.cmb_slot = c->pair_slot;
+  p.cmb_gates = c->gates;
   if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
     p.map_x = c->map_x_all;
     p.off_out = c->off_l;
@@ -884,12 +907,14 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.wr = wr;
   rp.x_in = c->x_in;
   rp.logits = c->logits;
+  rp.logits64 = c->logits64;
+  rp.ksplit = 1;
   rp.N = N;
   rp.E = E;
   rp.H = H;
   rp.k = k;
   rp.tpc = N <= 64 ? 4 : 8;  // tokens per CTA row of the route grid
-  if (const char* e = getenv("TIDE_ROUTE_TPC")) rp.tpc = std::max(1, std::min(8, atoi(e)));  // tuning
+  if (c->knob_route_tpc > 0) rp.tpc = c->knob_route_tpc;
   rp.norm_topk = (c->d.flags & TIDE_NORM_TOPK) ? 1 : 0;
   rp.maxN = c->maxN;
   rp.topk_idx = c->topk;
@@ -903,6 +928,8 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.g_cnt = c->g_cnt;
   rp.zero_i = c->ffn_ctrl;
   rp.n_zero = 2 + c->max_entries;
+  rp.zero_c = c->cmb_cnt;
+  rp.n_zero_c = c->ep ? 0 : N * ((H + kTileM - 1) / kTileM);
   rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
                                        : nullptr;
   rp.ep_P = 0;
@@ -923,12 +950,17 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   }
   // bf16 routers run phase 1 on the tensor cores (16 experts x 8 tokens per CTA);
   // TIDE_ROUTER_CC=1 forces the CUDA-core kernel (A/B measurement)
-  if (c->bf16 && E % 16 == 0 && H % 256 == 0 && !getenv("TIDE_ROUTER_CC")) {
+  if (c->bf16 && E % 16 == 0 && H % 256 == 0 && !c->knob_router_cc) {
     rp.tpc = 8;
-    const dim3 grid(E / 16, std::max(1, (N + 7) / 8));
+    // small batches: each 16-expert tile is split over 2 CTAs (half of H each, fp64 partials
+    // summed in phase 2) while the grid still fits one wave: half the bytes per SM
+    const int tiles = (E / 16) * std::max(1, (N + 7) / 8);
+    rp.ksplit = (c->logits64 && H % 512 == 0 && 2 * tiles <= c->num_sms && !c->knob_route_ksplit1)
+                    ? 2 : 1;
+    const dim3 grid((E / 16) * rp.ksplit, std::max(1, (N + 7) / 8));
     cudaError_t le;
     // large batches (more than one wave of 16 x 8 tiles): two CTAs per SM (<= 128 registers)
-    const bool two_per_sm = grid.x * grid.y > (unsigned)c->num_sms && !getenv("TIDE_ROUTE_ONE_PER_SM");
+    const bool two_per_sm = grid.x * grid.y > (unsigned)c->num_sms && !c->knob_route_one_per_sm;
 #define TC_LAUNCH(EP)                                                                        \
   le = two_per_sm ? launch_pdl(tide_route_tc_kernel<EP, 8, 2>, grid, dim3(kRouteThreads), 0, st, rp) \
                   : launch_pdl(tide_route_tc_kernel<EP, 8, 1>, grid, dim3(kRouteThreads), 0, st, rp)
@@ -1195,12 +1227,14 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     CU_TRY(cudaEventRecord(rec.ev[3], st));
   }
   // ---------------- a7/a9 FFN over the hit experts already in HBM (+ shared expert)
+  const bool fused_combine = !pool_mode && c->knob_fused_combine;
   if (N > 0) {
     s = launch_ffn(c, c->cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
                    c->ffn_ctrl + 1, N, st, false,
                    dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par,
                    !pool_mode,
-                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_item_trace) : nullptr);
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_item_trace) : nullptr,
+                   fused_combine ? out : nullptr);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
@@ -1221,8 +1255,8 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
 
-  // ---------------- a10 combine
-  if (N > 0) {
+  // ---------------- a10 combine (separate kernel when it is not fused into the FFN)
+  if (N > 0 && !fused_combine) {
     const dim3 grid(N, (H + 511) / 512);
     unsigned long long* ctr =  // debug: [6] latest start, [7] latest end in CTA 0's FFN record
         (dbg && dbg->ffn_trace) ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) + 6 : nullptr;
@@ -1457,6 +1491,68 @@ tide_status tide_optimize_interval(const tide_interval_model* m, int32_t* tau_ou
     if (tau == 1 || io + ms < best_c) {
       best = tau;
       best_c = io + ms;
+    }
+  }
+  *tau_out = best;
+  return TIDE_OK;
+}
+
+// NEXT-2 on B200: expert copies of a refresh interval measured on a routing trace.
+tide_status tide_interval_profile(const int32_t* counts, int32_t T, int32_t E, int32_t B,
+                                  double* miss_lag, double* mig_lag) {
+  if (!counts || !miss_lag || !mig_lag) return fail(TIDE_EINVAL, "null argument");
+  if (T < 1 || E < 1 || B < 1 || B > E) return fail(TIDE_EINVAL, "T %d / E %d / B %d", T, E, B);
+  // top-B of every step by (hits desc, id asc): the placement rule (R-8)
+  std::vector<uint8_t> top((size_t)T * E, 0);
+  std::vector<int> ids(E);
+  for (int t = 0; t < T; ++t) {
+    const int32_t* c = counts + (size_t)t * E;
+    for (int e = 0; e < E; ++e) ids[e] = e;
+    std::stable_sort(ids.begin(), ids.end(), [c](int a, int b) { return c[a] > c[b]; });
+    for (int i = 0; i < B; ++i) top[(size_t)t * E + ids[i]] = 1;
+  }
+  for (int j = 0; j < T; ++j) {
+    int64_t miss = 0, mig = 0;
+    for (int t = 0; t + j < T; ++t) {
+      const uint8_t* r = &top[(size_t)t * E];
+      const uint8_t* r2 = &top[(size_t)(t + j) * E];
+      const int32_t* c2 = counts + (size_t)(t + j) * E;
+      for (int e = 0; e < E; ++e) {
+        miss += (c2[e] > 0 && !r[e]);
+        mig += (r2[e] && !r[e]);
+      }
+    }
+    miss_lag[j] = (double)miss / (double)(T - j);
+    mig_lag[j] = (double)mig / (double)(T - j);
+  }
+  return TIDE_OK;
+}
+
+tide_status tide_interval_cost_trace(const tide_interval_trace_model* m, int32_t tau,
+                                     double* copies, double* cost) {
+  if (!m || !m->miss_lag || !m->mig_lag || !copies || !cost) return fail(TIDE_EINVAL, "null argument");
+  if (tau < 1 || tau >= m->T) return fail(TIDE_EINVAL, "tau %d outside [1, T-1 = %d]", tau, m->T - 1);
+  double per = m->mig_lag[tau];  // one interval: the refresh's promotions + tau steps of misses
+  for (int j = 0; j < tau; ++j) per += m->miss_lag[j];
+  *copies = (double)m->T / (double)tau * per;
+  *cost = m->c_io * *copies + (double)m->T * m->c_step;
+  return TIDE_OK;
+}
+
+tide_status tide_optimize_interval_trace(const tide_interval_trace_model* m, int32_t* tau_out,
+                                         double* curve) {
+  if (!m || !tau_out) return fail(TIDE_EINVAL, "null argument");
+  if (m->T < 2) return fail(TIDE_EINVAL, "T %d < 2", m->T);
+  int best = 1;
+  double best_c = 0.0;
+  for (int tau = 1; tau <= m->T - 1; ++tau) {  // Eq. 7 domain, exhaustive
+    double cp, c;
+    tide_status s = tide_interval_cost_trace(m, tau, &cp, &c);
+    if (s != TIDE_OK) return s;
+    if (curve) curve[tau - 1] = c;
+    if (tau == 1 || c < best_c) {
+      best = tau;
+      best_c = c;
     }
   }
   *tau_out = best;

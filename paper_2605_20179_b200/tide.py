@@ -32,7 +32,8 @@ EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert
             "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep",
             "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats",
             "tide_ctx_create_ep_p2p", "tide_ep_handle_bytes", "tide_ctx_ep_export",
-            "tide_ctx_ep_connect", "tide_ctx_ep_error")
+            "tide_ctx_ep_connect", "tide_ctx_ep_error", "tide_interval_profile",
+            "tide_interval_cost_trace", "tide_optimize_interval_trace")
 
 
 class TideError(RuntimeError):
@@ -83,6 +84,11 @@ class PhaseTimes(ctypes.Structure):
 class IntervalModel(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int32), ("B", ctypes.c_int32), ("d", ctypes.c_double),
                 ("c_io", ctypes.c_double), ("c_miss", ctypes.c_double)]
+
+
+class IntervalTraceModel(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int32), ("c_io", ctypes.c_double), ("c_step", ctypes.c_double),
+                ("miss_lag", ctypes.c_void_p), ("mig_lag", ctypes.c_void_p)]
 
 
 _lib = None
@@ -143,6 +149,13 @@ def lib():
                                          ctypes.POINTER(ctypes.c_void_p)]
         L.tide_ctx_ep_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.tide_ctx_ep_error.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
+        L.tide_interval_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        L.tide_interval_cost_trace.argtypes = [ctypes.POINTER(IntervalTraceModel), ctypes.c_int32,
+                                               ctypes.POINTER(ctypes.c_double),
+                                               ctypes.POINTER(ctypes.c_double)]
+        L.tide_optimize_interval_trace.argtypes = [ctypes.POINTER(IntervalTraceModel),
+                                                   ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -429,3 +442,44 @@ def trace_stats(counts, B: int, stream=None):
     _check(lib().tide_trace_stats(_ptr(counts.contiguous()), T, E, B, _ptr(sim), _ptr(uniq),
                                   _ptr(drift), _stream_ptr(stream)))
     return sim, uniq, drift[: T - 1]
+
+
+def interval_profile(counts, B: int):
+    """tide_interval_profile on a host [T, E] int32 array -> (miss_lag [T], mig_lag [T])."""
+    import numpy as np
+    c = np.ascontiguousarray(counts, np.int32)
+    T, E = c.shape
+    miss = np.zeros(T, np.float64)
+    mig = np.zeros(T, np.float64)
+    _check(lib().tide_interval_profile(ctypes.c_void_p(c.ctypes.data), T, E, B,
+                                       ctypes.c_void_p(miss.ctypes.data),
+                                       ctypes.c_void_p(mig.ctypes.data)))
+    return miss, mig
+
+
+def _trace_model(T, c_io, c_step, miss_lag, mig_lag):
+    import numpy as np
+    miss = np.ascontiguousarray(miss_lag, np.float64)
+    mig = np.ascontiguousarray(mig_lag, np.float64)
+    m = IntervalTraceModel(T, c_io, c_step, ctypes.c_void_p(miss.ctypes.data),
+                           ctypes.c_void_p(mig.ctypes.data))
+    return m, (miss, mig)
+
+
+def interval_cost_trace(T, c_io, c_step, miss_lag, mig_lag, tau):
+    """tide_interval_cost_trace -> (expert copies over the block, cost)."""
+    m, keep = _trace_model(T, c_io, c_step, miss_lag, mig_lag)
+    cp, c = ctypes.c_double(), ctypes.c_double()
+    _check(lib().tide_interval_cost_trace(ctypes.byref(m), tau, ctypes.byref(cp), ctypes.byref(c)))
+    return cp.value, c.value
+
+
+def optimize_interval_trace(T, c_io, c_step, miss_lag, mig_lag):
+    """tide_optimize_interval_trace -> (tau*, [cost for tau = 1..T-1])."""
+    import numpy as np
+    m, keep = _trace_model(T, c_io, c_step, miss_lag, mig_lag)
+    tau = ctypes.c_int32()
+    curve = np.zeros(max(1, T - 1), np.float64)
+    _check(lib().tide_optimize_interval_trace(ctypes.byref(m), ctypes.byref(tau),
+                                              ctypes.c_void_p(curve.ctypes.data)))
+    return tau.value, curve

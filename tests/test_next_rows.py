@@ -161,3 +161,54 @@ def test_counter_window_and_cumulative_sums():
         if mode == 2:
             assert (keys[2] == h[0] + h[1]).all() and (keys[4] == h[0] + h[1] + h[2] + h[3]).all()
             assert (acc == sum(h)).all()
+
+
+# ------------------------------------------------------------------ NEXT-2 on B200 (trace model)
+def test_interval_trace_model_hand_worked():
+    """Oracle and library vs the hand-worked example (tests/golden/interval_trace_example.json)."""
+    from paper_2605_20179_b200 import _build
+    _build.build()
+    from paper_2605_20179_b200 import tide
+    ex = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                     "interval_trace_example.json")))
+    c = np.array(ex["counts"], np.int32)
+    T = c.shape[0]
+    for miss, mig in (oracle.interval_profile(c, ex["B"]), tide.interval_profile(c, ex["B"])):
+        assert np.allclose(miss, ex["miss_lag"], rtol=0, atol=1e-15)
+        assert np.allclose(mig, ex["mig_lag"], rtol=0, atol=1e-15)
+        for tau, want in ex["copies"].items():
+            assert oracle.interval_copies_trace(T, int(tau), miss, mig) == pytest.approx(want, abs=1e-12)
+            cp, cost = tide.interval_cost_trace(T, 2.0, 0.5, miss, mig, int(tau))
+            assert cp == pytest.approx(want, abs=1e-12) and cost == pytest.approx(2 * want + T * 0.5)
+        assert tide.optimize_interval_trace(T, 1.0, 0.0, miss, mig)[0] == ex["tau_star"]
+
+
+def test_interval_trace_model_invariants():
+    """A constant trace never migrates and misses the same experts at every lag (copies do not
+    depend on tau, so tau* = 1 by the tie rule); B = E never misses or migrates."""
+    rng = np.random.default_rng(5)
+    row = rng.integers(0, 4, 24).astype(np.int32)
+    c = np.tile(row, (10, 1))
+    miss, mig = oracle.interval_profile(c, 6)
+    assert (mig == 0).all() and np.allclose(miss, miss[0])
+    assert miss[0] == ((row > 0).sum() - min(6, (row > 0).sum()))
+    copies = [oracle.interval_copies_trace(10, t, miss, mig) for t in range(1, 10)]
+    assert np.allclose(copies, 10 * miss[0])
+    miss, mig = oracle.interval_profile(rng.integers(0, 3, (8, 24)).astype(np.int32), 24)
+    assert (miss == 0).all() and (mig == 0).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_library_interval_trace_matches_oracle(seed):
+    from paper_2605_20179_b200 import tide
+    rng = np.random.default_rng(100 + seed)
+    T, E = int(rng.integers(2, 40)), int(rng.integers(2, 300))
+    B = int(rng.integers(1, E + 1))
+    c = rng.poisson(rng.uniform(0.1, 3), (T, E)).astype(np.int32)
+    m1, g1 = oracle.interval_profile(c, B)
+    m2, g2 = tide.interval_profile(c, B)
+    assert (m1 == m2).all() and (g1 == g2).all()
+    tau, curve = tide.optimize_interval_trace(T, 1e-4, 1e-5, m2, g2)
+    ref = [1e-4 * oracle.interval_copies_trace(T, t, m1, g1) + T * 1e-5 for t in range(1, T)]
+    assert np.allclose(curve, ref, rtol=1e-12)
+    assert tau == 1 + int(np.argmin(ref))

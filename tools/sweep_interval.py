@@ -1,18 +1,25 @@
 """BJ.configs[4]: refresh-interval x capacity sweep on the mini shape with a batch of 8 blocks
-(256 tokens per layer-step), pinned-host serving of non-resident experts.
+(256 tokens per layer-step), pinned-host serving of non-resident experts, and the NEXT-2
+models against it.
 
 For every (capacity C, interval tau): one full block (T = 32 steps) of layer-steps on
-`--layers` layers, timed with CUDA events; H2D copies from the library's stats.  Then the
-NEXT-2 model: drift d measured on the GPU (tide_trace_stats, Eq. 4, top-C of each step's
-hits), c_io = c_miss = measured seconds per expert H2D copy (a miss streams the expert,
-R-13), tau* from tide_optimize_interval, compared with the measured best tau per C.
-usage: python tools/sweep_interval.py [--layers 2] [--out profiles/r01/sweep_interval.json]
+`--layers` layers, timed with CUDA events; expert H2D copies from the library's stats.
+Models (both host-side in libtide.so, both pinned against the oracle):
+  paper  (Eq. 5-7, tide_optimize_interval): drift d measured on the GPU routing trace
+         (tide_trace_stats, Eq. 4), c_io = c_miss = measured seconds per expert H2D copy
+  trace  (DESIGN R-21, tide_interval_profile + tide_optimize_interval_trace): the expert
+         copies of each tau computed from the same trace's miss/migration lag curves,
+         including the experts that stream at every step (hit but outside even a fresh
+         top-C), cost = c_io * copies + T * c_step with c_step = the measured step time at
+         C = E (same mode, no expert I/O after the first copies).
+The routing trace does not depend on C or tau (outputs are lossless; routing is a function
+of the inputs), so one trace per layer serves every cell.
+usage: python tools/sweep_interval.py [--layers 2] [--out profiles/r02/sweep_interval.json]
 """
 import argparse
 import json
 import os
 import sys
-import time
 
 import numpy as np
 import torch
@@ -24,8 +31,8 @@ from paper_2605_20179_b200 import tide  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=2)
 ap.add_argument("--caps", default="64,128,192,256")
-ap.add_argument("--taus", default="1,2,4,8,16")
-ap.add_argument("--out", default="profiles/r01/sweep_interval.json")
+ap.add_argument("--taus", default="1,2,3,4,6,8,12,16")
+ap.add_argument("--out", default="profiles/r02/sweep_interval.json")
 a = ap.parse_args()
 s = g.SWEEP
 E, k, H, F, N, T = s.num_experts, s.top_k, s.hidden, s.ffn, s.tokens, s.steps
@@ -44,9 +51,8 @@ for l in range(a.layers):
                        x=g.block_hidden_torch(s, 7, l, dev)))
 # measured H2D cost of one expert (pinned -> HBM)
 buf = torch.empty(xb // 2, dtype=torch.bfloat16, device=dev)
-src = layers[0]["host"][0]
 for _ in range(3):
-    buf.copy_(src, non_blocking=True)
+    buf.copy_(layers[0]["host"][0], non_blocking=True)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -57,57 +63,86 @@ torch.cuda.synchronize()
 c_io = e0.elapsed_time(e1) / 1e3 / 20
 print(f"H2D per expert {c_io * 1e6:.1f} us ({xb / c_io / 1e9:.1f} GB/s)", flush=True)
 
-# routing trace of layer 0 over the block (device_all run, interval 1) -> drift per capacity
-ctx = tide.Context(desc, E)
-dall = layers[0]["host"].to(dev)
-counts = torch.empty(T, E, dtype=torch.int32, device=dev)
-pl = torch.zeros(E, dtype=torch.uint8, device=dev)
-for t in range(T):
-    ctx.moe_step(layers[0]["x"][t], layers[0]["wr"], device_all=dall, shared_w=layers[0]["shared"],
-                 placement=pl, step=t, interval=1, hit_counts=counts[t])
-del dall
-torch.cuda.empty_cache()
+# routing trace of every layer over the block (device_all run)
+traces = []
+for L in layers:
+    ctx = tide.Context(desc, E)
+    dall = L["host"].to(dev)
+    counts = torch.empty(T, E, dtype=torch.int32, device=dev)
+    pl = torch.zeros(E, dtype=torch.uint8, device=dev)
+    for t in range(T):
+        ctx.moe_step(L["x"][t], L["wr"], device_all=dall, shared_w=L["shared"], placement=pl,
+                     step=t, interval=1, hit_counts=counts[t])
+    torch.cuda.synchronize()
+    traces.append(counts)
+    del dall, ctx
+    torch.cuda.empty_cache()
 
 res = {"workload": "BJ.configs[4]: mini shape, 8 blocks (256 tokens) per layer-step, "
-                   f"{a.layers} layers, T={T}, pinned-host serving (host_master)",
+                   f"{a.layers} layers, T={T}, pinned-host serving (host_master), calibrated routing",
        "h2d_us_per_expert": c_io * 1e6, "runs": [], "model": []}
+taus = [int(v) for v in a.taus.split(",")]
 for C in [int(v) for v in a.caps.split(",")]:
-    sim, uq, drift = tide.trace_stats(counts, C)
-    d = float(drift.mean().item())
-    tau_star, curve = tide.optimize_interval(T, C, d, c_io, c_io)
-    res["model"].append({"capacity": C, "drift_mean": d, "tau_star": tau_star,
-                         "curve_ms": [round(v * 1e3, 3) for v in curve[:16]]})
-    for tau in [int(v) for v in a.taus.split(",")]:
+    for tau in taus:
         ctxs = [tide.Context(desc, C, 16) for _ in layers]
         pls = [torch.zeros(E, dtype=torch.uint8, device=dev) for _ in layers]
-        stats = dict(copies=0, h2d=0, resident_pairs=0, pairs=0)
+        st = dict(copies=0, h2d=0, resident_pairs=0, pairs=0)
         torch.cuda.synchronize()
         e0.record()
         for t in range(T):
             for L, c, p in zip(layers, ctxs, pls):
                 r = c.moe_step(L["x"][t], L["wr"], host_master=L["host"], shared_w=L["shared"],
                                placement=p, step=t, interval=tau, placement_out=p, stats=True)
-                stats["copies"] += r.stats["copies"]
-                stats["h2d"] += r.stats["h2d_bytes"]
-                stats["resident_pairs"] += r.stats["resident_pairs"]
-                stats["pairs"] += N * k
+                st["copies"] += r.stats["copies"]
+                st["h2d"] += r.stats["h2d_bytes"]
+                st["resident_pairs"] += r.stats["resident_pairs"]
+                st["pairs"] += N * k
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         ls = T * len(layers)
         row = {"capacity": C, "interval": tau, "ms_per_layer_step": ms / ls,
                "block_tokens_per_s": N * ls / (ms / 1e3),
-               "h2d_experts_per_layer_step": stats["copies"] / ls,
-               "h2d_GBps": stats["h2d"] / (ms / 1e3) / 1e9,
-               "resident_pair_rate": stats["resident_pairs"] / stats["pairs"]}
+               "h2d_experts_per_layer_step": st["copies"] / ls,
+               "h2d_GBps": st["h2d"] / (ms / 1e3) / 1e9,
+               "resident_pair_rate": st["resident_pairs"] / st["pairs"]}
         res["runs"].append(row)
         print(json.dumps(row), flush=True)
         del ctxs
+
+# the step without expert I/O: the C = E run minus its (cold-start) copies at the H2D rate
+ref = next(r for r in res["runs"] if r["capacity"] == E and r["interval"] == 1)
+c_step = max(0.0, ref["ms_per_layer_step"] / 1e3 - c_io * ref["h2d_experts_per_layer_step"])
 for C in [int(v) for v in a.caps.split(",")]:
-    rows = [r for r in res["runs"] if r["capacity"] == C]
-    best = max(rows, key=lambda r: r["block_tokens_per_s"])
-    m = [x for x in res["model"] if x["capacity"] == C][0]
-    m["measured_best_tau"] = best["interval"]
+    rows = {r["interval"]: r for r in res["runs"] if r["capacity"] == C}
+    best = min(rows.values(), key=lambda r: r["ms_per_layer_step"])
+    near = sorted(t for t, r in rows.items() if r["ms_per_layer_step"] <= 1.01 * best["ms_per_layer_step"])
+    # paper model (Eq. 5-7) with the mean drift over the layers' traces
+    d = float(np.mean([tide.trace_stats(tr, C)[2].mean().item() for tr in traces]))
+    tau_p, curve_p = tide.optimize_interval(T, C, d, c_io, c_io)
+    # trace model: lag profiles averaged over the layers
+    prof = [tide.interval_profile(tr.cpu().numpy(), C) for tr in traces]
+    miss = np.mean([p[0] for p in prof], axis=0)
+    mig = np.mean([p[1] for p in prof], axis=0)
+    tau_t, curve_t = tide.optimize_interval_trace(T, c_io, c_step, miss, mig)
+    cells = []
+    for tau in taus:
+        cp, cost = tide.interval_cost_trace(T, c_io, c_step, miss, mig, tau)
+        meas = rows[tau]
+        cells.append({"interval": tau,
+                      "copies_per_step_model": round(cp / T, 2),
+                      "copies_per_step_measured": round(meas["h2d_experts_per_layer_step"], 2),
+                      "ms_per_step_model": round(cost / T * 1e3, 3),
+                      "ms_per_step_measured": round(meas["ms_per_layer_step"], 3),
+                      "cost_rel_err": round(cost / T * 1e3 / meas["ms_per_layer_step"] - 1, 4)})
+    res["model"].append({
+        "capacity": C, "measured_best_tau": best["interval"],
+        "measured_within_1pct_of_best": near,
+        "paper_eq5_7": {"drift_mean": d, "tau_star": tau_p,
+                        "curve_ms_per_step": [round(v / T * 1e3, 3) for v in curve_p[:16]]},
+        "trace_model": {"tau_star": tau_t, "c_step_ms": round(c_step * 1e3, 3),
+                        "always_streamed_per_step": round(float(miss[0]), 2),
+                        "cells": cells}})
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"), indent=1)
 print(json.dumps(res["model"]))
