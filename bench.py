@@ -86,6 +86,9 @@ def parse():
     ap.add_argument("--prefetch-mb", type=float, default=-1,
                     help="NEXT-3 cross-layer L2 prefetch budget per layer-step (MB); "
                          "-1 = default (32 MB when all experts are in HBM), 0 = off")
+    ap.add_argument("--h2d-prefetch", type=int, default=0,
+                    help="NEXT-3 H2D prefetch with pinned-host serving: experts per layer copied "
+                         "ahead into the next layer's prefetch slots (0 = off)")
     ap.add_argument("--ep", action="store_true",
                     help="expert parallelism over the ranks (default at N>1; also at N=1)")
     ap.add_argument("--p2p", action="store_true",
@@ -371,6 +374,14 @@ class Stack:
             L["ctx"].set_prefetch(nx["ctx"] if mb > 0 else None, nx["w"] if mb > 0 else None,
                                   int(mb * 1e6))
 
+    def set_h2d_prefetch(self, n_experts: int):
+        """NEXT-3 H2D prefetch (pinned-host serving): each layer's step copies the next
+        layer's predicted streamed experts into that layer's prefetch slots."""
+        Ly = len(self.layers)
+        for li, L in enumerate(self.layers):
+            nx = self.layers[(li + 1) % Ly]
+            L["ctx"].set_prefetch(nx["ctx"], None, n_experts * self.s.expert_bytes)
+
     def layer_step(self, L, t, x=None, stats=False):
         xx = L["x"][t] if x is None else x
         a = self.args
@@ -557,7 +568,7 @@ def phase_sums(phases):
 
 # ------------------------------------------------------------------ single device
 def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=None, full=True,
-                   steps=None, warmup=None):
+                   steps=None, warmup=None, h2d_prefetch=None):
     """One single-device (or replica) run of stack `s` at capacity `cap`: value, roofline
     and, with `full`, clocks / e2e / step split / the prefetch-off control."""
     steps = steps or args.steps
@@ -569,6 +580,9 @@ def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=Non
     pf_mb = args.prefetch_mb if args.prefetch_mb >= 0 else (32.0 if not pool else 0.0)
     if pf_mb > 0 and not pool:
         st.set_prefetch(pf_mb)
+    h2d_pf = args.h2d_prefetch if h2d_prefetch is None else h2d_prefetch
+    if pool and h2d_pf > 0:
+        st.set_h2d_prefetch(h2d_pf)
     for i in range(warmup):
         st.step(i)
     torch.cuda.synchronize()
@@ -587,7 +601,8 @@ def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=Non
            "workload": workload_str(s, cap, args.interval),
            "launch": "CUDA graph per block step (all layers), replayed" if graphs
                      else "eager stream (PDL-chained kernels)",
-           "prefetch_mb": pf_mb, "gpu_launches": launches, "steps": steps, "warmup": warmup,
+           "prefetch_mb": pf_mb, "h2d_prefetch_experts": h2d_pf if pool else 0,
+           "gpu_launches": launches, "steps": steps, "warmup": warmup,
            "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()},
            "ms_per_step_with_phase_events": round(ms_ph / steps, 4)}
     if full:
@@ -683,9 +698,10 @@ def sub_results(args, dev):
                               tide.TIDE_BF16)
         w = [gen_layer(args, fs, l, dev, desc, host=True) for l in range(fs.layers)]
         for cap in (64, 217):
-            out[f"flash_C{cap}_8layers"] = measure_single(args, fs, cap, dev, weights=w,
-                                                          full=False, steps=max(3, steps // 2),
-                                                          warmup=warmup)
+            for pf in (0, 8):  # NEXT-3 H2D prefetch off / on (8 experts per layer)
+                out[f"flash_C{cap}_8layers" + ("_h2d_prefetch" if pf else "")] = measure_single(
+                    args, fs, cap, dev, weights=w, full=False, steps=max(3, steps // 2),
+                    warmup=warmup, h2d_prefetch=pf)
         del w
     except Exception as e:
         out["flash_pinned_host"] = {"error": repr(e)[:300]}

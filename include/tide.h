@@ -282,6 +282,14 @@ TIDE_API tide_status tide_ctx_ep_connect(tide_ctx* ctx, const void* handles,
                                          const void* const* bases);
 /* *err = 1 if a peer-memory wait timed out since the context was created (synchronous). */
 TIDE_API tide_status tide_ctx_ep_error(tide_ctx* ctx, int32_t* err);
+/* Failure handling of an expert-parallel context (either exchange), host side: waits until
+ * the context's last step has completed on the device, polling every ~50 us.  NCCL
+ * contexts: an asynchronous communicator error (ncclCommGetAsyncError) or no completion
+ * within `timeout_ms` aborts the communicator (ncclCommAbort: the collectives in flight
+ * return, the context is unusable afterwards) and returns TIDE_ENCCL.  Peer-memory
+ * contexts: a kernel-side wait that gave up (the error word) returns TIDE_ECUDA; no
+ * completion within `timeout_ms` returns TIDE_ECUDA.  TIDE_OK when the step completed.  */
+TIDE_API tide_status tide_ctx_ep_wait(tide_ctx* ctx, int32_t timeout_ms);
 
 /* Per-phase device timing (CUDA events recorded on the step's stream at phase
  * boundaries).  Enabling resets the accumulators; tide_ctx_get_timing waits
@@ -304,16 +312,29 @@ TIDE_API tide_status tide_ctx_get_timing(tide_ctx* ctx, tide_phase_times* out);
  * NEXT-3: cross-layer L2 prefetch (P:278-281's "overlap" intent).
  * After this call, every device_all tide_moe_step on `ctx` ends its FFN by prefetching
  * into L2 (cp.async.bulk.prefetch.L2) the experts of `next` most likely to be hit at
- * next's coming step: next's experts with hits > 0 at its most recent step, ranked by
- * (hits desc, id asc) by next's own bookkeeping kernel, up to budget_bytes. Each CTA
- * of the persistent FFN issues its share once it has no more work, so the prefetch fills
- * the FFN tail, the combine and next's routing, when HBM would otherwise be idle.
+ * next's coming step: the shared expert, then next's experts with hits > 0 at its most
+ * recent step in ascending id (the order next's FFN claims them; TIDE_PF_BY_HITS=1 ranks
+ * by hits instead), their gate/up rows (what the FFN's first items read) up to
+ * budget_bytes. Each CTA of the persistent FFN issues its share once it has no more
+ * work, so the prefetch fills the FFN tail, the combine and next's routing, when HBM
+ * would otherwise be idle.
  *   next:            the context of the layer called after `ctx` (same device); NULL or
  *                    budget_bytes == 0 disables. `next` must outlive `ctx` or be unset.
- *   next_device_all: the packed experts `next` is called with ([E, 3HF], device).
- * It is a cache hint only: outputs are bitwise unchanged. Nothing is prefetched before
- * `next` has run one step. Returns TIDE_EINVAL on a null ctx, negative budget,
- * different devices, or next != NULL with next_device_all == NULL.
+ *   next_device_all: the packed experts `next` is called with ([E, 3HF], device), or
+ *                    NULL when `next` serves its experts from a pinned host master
+ *                    (host_master): then, at the end of every host_master step of `ctx`,
+ *                    the experts next streamed at its previous step (hit, not in HBM;
+ *                    most-hit first, up to budget_bytes / expert bytes, at most 64) are
+ *                    copied host-to-HBM into `next`'s own prefetch slots on its side
+ *                    stream, so the H2D link works through the gap before next's step
+ *                    plans its copies; next's step computes those experts from the
+ *                    prefetch slots (or moves a promoted one HBM-to-HBM) instead of
+ *                    copying them again.  The slots are extra HBM owned by `next`; set this
+ *                    before next's first host_master step.  Prefetch copies are counted in
+ *                    next's stats (copies, h2d_bytes), wrong predictions included.
+ * It is a cache / copy-timing hint only: outputs are bitwise unchanged. Nothing is
+ * prefetched before `next` has run one step. Returns TIDE_EINVAL on a null ctx, negative
+ * budget, different devices, or a host prefetch set after next's first host step.
  * ------------------------------------------------------------------------ */
 TIDE_API tide_status tide_ctx_set_prefetch(tide_ctx* ctx, tide_ctx* next,
                                            const void* next_device_all, int64_t budget_bytes);

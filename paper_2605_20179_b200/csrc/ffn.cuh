@@ -57,6 +57,8 @@ struct FfnParams {
   const int* pf_n;         // number of ranked (hit) experts
   int pf_max;              // budget in experts
   long long pf_xb;         // bytes per packed expert
+  long long pf_span;       // bytes prefetched per expert, from its start (<= pf_xb)
+  const uint8_t* pf_shared;  // nullable: next layer's shared expert (prefetched first)
   const int* slot_of;    // [E] pool slot (nullptr: slot = e)
   int* off_out;          // [E] row offsets written by CTA 0 (build mode; read by combine)
   const int4* entries;   // global mode: host-built list
@@ -316,10 +318,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     const uint64_t pol_w = policy_evict_first(), pol_a = policy_evict_last();
     int stage = 0, islot = 0;
     uint32_t sphase = 0, iphase = 0;
+    bool first = true;
     while (true) {
-      int it = 0;
-      if (lane == 0) it = atomicAdd(p.sched, 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
+      // item i of the first wave is CTA i's (no counter round trip before the first loads);
+      // every later item comes from the shared counter, offset past the first wave
+      int it = blockIdx.x;
+      if (!first) {
+        if (lane == 0) it = (int)gridDim.x + atomicAdd(p.sched, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+      }
+      first = false;
       unsigned long long* itr = (p.itrace && n_items < 64)
                                     ? p.itrace + 4 * (64 * (size_t)blockIdx.x + n_items) : nullptr;
       if (itr && lane == 0) itr[0] = globaltimer_ns();
@@ -420,21 +428,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     }
     if (tr && lane == 0) { tr[2] = globaltimer_ns(); tr[4] = n_items; }
     // NEXT-3 cross-layer prefetch: this CTA has no more work, so its share of the next
-    // layer's most-hit experts (ranked by that layer's book at its previous step) is pulled
-    // into L2 while the FFN drains and the combine / next routing leave HBM idle.
-    // Piece i of the ranked byte range goes to CTA i % grid, so the first CTAs to finish
-    // cover the highest-ranked experts first.  A cache hint only: values are unaffected.
+    // layer's likely experts (that layer's hit experts at its previous step, in the order its
+    // FFN claims them: the shared expert, then ascending id) is pulled into L2 while the FFN
+    // drains and the combine / next routing leave HBM idle.  Piece i of the byte range goes
+    // to CTA i % grid, so the first CTAs to finish cover the first-claimed experts first.
+    // A cache hint only: values are unaffected.
     if (p.pf_base) {
-      const int n = min(__ldcg(p.pf_n), p.pf_max);
-      const long long ppe = (p.pf_xb + kPfPiece - 1) / kPfPiece;
+      const int sh = p.pf_shared ? 1 : 0;
+      const int n = min(__ldcg(p.pf_n) + sh, p.pf_max);
+      const long long ppe = (p.pf_span + kPfPiece - 1) / kPfPiece;
       const long long pieces = (long long)n * ppe;
       for (long long i = blockIdx.x + (long long)gridDim.x * lane; i < pieces;
            i += (long long)gridDim.x * 32) {
         const int j = (int)(i / ppe);
         const long long q = (i - (long long)j * ppe) * kPfPiece;
-        const int e = __ldcg(p.pf_list + j);
-        const uint32_t bytes = (uint32_t)min((long long)kPfPiece, p.pf_xb - q);
-        prefetch_l2_bulk(p.pf_base + (size_t)e * p.pf_xb + q, bytes);
+        const uint8_t* src = (j < sh) ? p.pf_shared
+                                      : p.pf_base + (size_t)__ldcg(p.pf_list + j - sh) * p.pf_xb;
+        const uint32_t bytes = (uint32_t)min((long long)kPfPiece, p.pf_span - q);
+        prefetch_l2_bulk(src + q, bytes);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -503,6 +514,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       if (lane == 0) mbar_arrive(&iempty[islot]);
       if (++islot == kItemSlots) { islot = 0; iphase ^= 1; }
       if (item.kind < 0) break;
+      // EP: the first 16 rows' destinations are fetched while the MMAs still run
+      unsigned d0[16];
+      if (EP && item.kind == 1 && !(item.flags & 2)) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)  // same address in every thread: broadcast loads
+          d0[i] = i < item.m ? __ldg(p.ep_dst + item.tokbase + i) : 0u;
+      }
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)acc * 256u;
@@ -530,7 +548,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
           unsigned d[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i)  // same address in every thread: broadcast loads
-            d[i] = c0 + i < item.m ? __ldg(p.ep_dst + item.tokbase + c0 + i) : 0u;
+            d[i] = c0 == 0 ? d0[i] : (c0 + i < item.m ? __ldg(p.ep_dst + item.tokbase + c0 + i) : 0u);
           tmem_ld16(tbase + c0, v);
           if (h < H) {
 #pragma unroll
@@ -578,8 +596,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
                (int)gridDim.x - 1;
     }
     __syncthreads();
-    if (s_last) {  // the grid's last CTA: counts to every rank, one system fence, arrive
-      __threadfence();
+    if (s_last) {  // the grid's last CTA: counts to every rank, one system release, arrive
       for (int i = threadIdx.x; i < p.ep_P * p.ep_El; i += blockDim.x) {
         const int dst = i / p.ep_El, e = i - dst * p.ep_El;
         reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_hits)[p.ep_e0 + e] = __ldcg(p.ep_cnt_l + e);
@@ -587,11 +604,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       __syncthreads();
       if (threadIdx.x == 0) {
         const int par = __ldcg(p.ep_par);
-        __threadfence_system();
+        fence_release_sys();
         for (int dst = 0; dst < p.ep_P; ++dst)
-          asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(
-                           reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par),
-                       "r"(1u) : "memory");
+          red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par, 1u);
       }
     }
   }

@@ -76,6 +76,14 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Release pattern at system scope: one fence (MEMBAR.ALL.SYS) ordering every prior write of
+// the thread (and, cumulatively, those it acquired) before the relaxed arrivals after it.
+__device__ __forceinline__ void fence_release_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void red_relaxed_sys_add_u32(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // The same arrival at system scope: used by CTAs that stored into a peer GPU's memory, so
 // their own release (MEMBAR.ALL.SYS, no sequentially-consistent fence) covers those stores
 // before anyone downstream can observe the arrival.

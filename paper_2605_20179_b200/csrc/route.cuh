@@ -108,6 +108,7 @@ struct BookParams {
   const int* par;       // nullable: cnt is double-buffered, this step's half = par^1
   int* pf_list;         // nullable (NEXT-3): experts with hits > 0 ranked by (hits desc, id asc)
   int* pf_n;            //   and their number; read by the previous layer's FFN next step
+  int pf_by_hits;       //   rank by (hits desc, id asc) instead of by id
   const unsigned* mask; // [E * NW]
   unsigned* mask_rw;    // same, zeroed after use
   const int* topk_idx;  // [N,k]
@@ -231,19 +232,23 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
     int my_e = 0;
     float my_l = 0.f;
     for (int j = 0; j < k; ++j) {
-      // warp argmax of the lane heads by (value desc, id asc): max key, then min id among
-      // the lanes holding it (two redux.sync instead of a 5-step shuffle butterfly)
+      // warp argmax of the lane heads by (value desc, id asc): max key (redux.sync); the lane
+      // holding it from a ballot, and only when several lanes hold it (an exact tie) the
+      // lowest id among them (a second redux.sync; warp-uniform branch)
       const unsigned hk = order_key(v[0]);
       const unsigned mk = __reduce_max_sync(0xffffffffu, hk);
-      const int bi = (int)__reduce_min_sync(0xffffffffu, hk == mk ? (unsigned)id[0] : 0xffffffffu);
-      const float bv = key_value(mk);
-      if ((bi & 31) == lane) {
+      const unsigned held = __ballot_sync(0xffffffffu, hk == mk);
+      int w = __ffs(held) - 1;
+      if (held & (held - 1))
+        w = (int)__reduce_min_sync(0xffffffffu, hk == mk ? (unsigned)id[0] : 0xffffffffu) & 31;
+      const int bi = __shfl_sync(0xffffffffu, id[0], w);  // off the next round's chain
+      if (lane == w) {
 #pragma unroll
         for (int i = 0; i + 1 < EPL; ++i) { v[i] = v[i + 1]; id[i] = id[i + 1]; }
         v[EPL - 1] = -INFINITY;
         id[EPL - 1] = 0x7fffffff;
       }
-      if (lane == j) { my_e = bi; my_l = bv; }
+      if (lane == j) { my_e = bi; my_l = key_value(mk); }
     }
     float denom = z;  // gates (R-2)
     if (p.norm_topk) {
@@ -352,15 +357,14 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
-      if (p.ep_P) {  // every CTA's peer stores precede this point through the gpu-scope
-                     // g_cnt / g_done chains; one system-scope fence publishes them: arrive
+      if (p.ep_P) {  // every CTA's peer stores precede this point (each CTA released them
+                     // itself at world > 1; the g_cnt / g_done chains acquired them here):
+                     // one release fence at system scope, then the arrivals
         for (int dst = 0; dst < p.ep_P; ++dst)
           reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
-        __threadfence_system();
+        fence_release_sys();
         for (int dst = 0; dst < p.ep_P; ++dst)
-          asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(
-                           reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + (par ^ 1)),
-                       "r"(1u) : "memory");
+          red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + (par ^ 1), 1u);
       }
     }
   }
@@ -592,13 +596,15 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
   }
   __syncthreads();
   if (p.pf_list) {  // NEXT-3: rank this step's hit experts for the previous layer's prefetch
+    // by id (the FFN's claim order: the prefetched experts are the ones its first wave
+    // streams) or by hits (pf_by_hits)
     for (int e = tid; e < E; e += blockDim.x) {
       const int he = s_hits[e];
       if (he > 0) {
         int r = 0;
         for (int f = 0; f < E; ++f) {
           const int hf = s_hits[f];
-          r += (hf > he) || (hf == he && f < e);
+          r += p.pf_by_hits ? ((hf > he) || (hf == he && f < e)) : (hf > 0 && f < e);
         }
         p.pf_list[r] = e;  // hit experts occupy ranks 0..U-1
       }
@@ -701,22 +707,27 @@ __global__ void __launch_bounds__(1024) tide_book_kernel(const __grid_constant__
 }
 
 // ---------------------------------------------------------------- a10 combine
-// grid (N, ceil(H / 512)), 128 threads x 4 columns.  row(n,j) = off[e] + slot(n,j).
+// grid (N, ceil(H / 512)), 128 threads x 4 columns.  row(n,j) = off[e] + slot(n,j), with
+// off[e] = the counts of the experts before e in id order (the FFN's row rule).
 // fp32 FMA over j in slot order (then the shared expert), one rounding (R-14).
 template <typename T>
 __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restrict__ y,
                                                            const float* __restrict__ gates,
                                                            const int* __restrict__ topk,
                                                            const int* __restrict__ pair_slot,
-                                                           const int* __restrict__ off,
+                                                           const int* __restrict__ cnt2,
+                                                           const int* __restrict__ par, int E,
                                                            T* __restrict__ out, int N, int k,
                                                            int H, int shared,
                                                            unsigned long long* trace) {
+  __shared__ int s_off[1024];
+  __shared__ int s_scratch[33];
   const int n = blockIdx.x, lane = threadIdx.x & 31;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  // lane j < k fetches pair j's expert, slot and gate before the wait: the route kernel that
-  // wrote them completed before the FFN (the preceding grid) triggered this launch; off[]
-  // and y come from the FFN itself, after the wait
+  // Everything from the route kernel is read before the wait: it completed before the FFN
+  // (the preceding grid) triggered this launch.  Lane j < k fetches pair j's expert, slot and
+  // gate; the CTA scans the per-expert counts into the row offsets off[] (one L2 round trip
+  // and a CTA scan that overlap the FFN's tail).  Only y comes from the FFN, after the wait.
   int e_j = 0, s_j = 0, r_j = 0;
   float g_j = 0.f;
   if (lane < k) {
@@ -725,10 +736,16 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
     s_j = __ldcg(pair_slot + q);
     g_j = __ldcg(gates + q);
   }
+  {
+    const int* cnt = cnt2 + (__ldcg(par) ^ 1) * E;  // this step's half (route.cuh RouteParams)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_off[e] = __ldcg(cnt + e);
+    __syncthreads();
+    block_scan_excl(s_off, E, s_scratch);
+  }
   pdl_wait();
   pdl_trigger();
   if (trace && threadIdx.x == 0) atomicMax(trace, globaltimer_ns());  // debug: latest start
-  if (lane < k) r_j = __ldcg(off + e_j) + s_j;
+  if (lane < k) r_j = s_off[e_j] + s_j;
   const bool valid = c < H;  // (lanes stay converged for the shuffles)
   const int cc = valid ? c : 0;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);

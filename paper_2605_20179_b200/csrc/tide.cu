@@ -18,10 +18,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -128,6 +130,16 @@ struct tide_ctx {
   tide_ctx* pf_next = nullptr;         // the layer this context prefetches for
   const void* pf_weights = nullptr;    // its packed experts (device_all)
   int pf_max = 0;                      // budget in experts
+  int64_t pf_budget = 0;               // budget in bytes
+  // NEXT-3 H2D prefetch (host_master mode)
+  tide_ctx* pf_next_h = nullptr;       // the layer this context prefetches host experts for
+  int pf_slots_req = 0;                // prefetch slots of this context (set before its pool)
+  std::vector<int> pf_exp;             // expert in each prefetch slot (-1 free)
+  std::vector<cudaEvent_t> pf_ev;      // its H2D copy done
+  cudaEvent_t ev_pf_free = nullptr;    // this context's last step is done with the slots
+  std::vector<int> last_streamed;      // experts streamed at the last step, most-hit first
+  const void* last_master = nullptr;   // the host master of the last step
+  int pf_issued = 0;                   // H2D copies issued for this context's next step
   int* list = nullptr;       // [E * maxN] per-expert token lists
   unsigned* mask = nullptr;  // [E * NWmax] per-expert token bitmasks
   int* g_cnt = nullptr;      // [maxN + 2] route-kernel last-CTA counters
@@ -146,6 +158,8 @@ struct tide_ctx {
   int knob_route_tpc = 0;
   bool knob_router_cc = false, knob_route_one_per_sm = false, knob_fused_combine = false;
   bool knob_route_ksplit1 = false;  // TIDE_ROUTE_KSPLIT1=1: one router CTA per 16 x 8 tile
+  bool knob_pf_by_hits = false;    // TIDE_PF_BY_HITS=1: prefetch ranked by hits, no shared expert
+  bool knob_pf_whole = false;      // TIDE_PF_WHOLE_EXPERT=1: prefetch whole experts (not gate/up)
   double* logits64 = nullptr;       // [2][maxN][E] fp64 router partials (bf16, TC router)
   int* ffn_ctrl = nullptr;   // [2 + max_entries]: scheduler counter, per-entry done counters,
                              // grid arrival counter (peer-memory EP)
@@ -200,6 +214,7 @@ struct tide_ctx {
   EpSymLayout lay{};
   EpPeers peers{};
   std::vector<void*> ipc_opened;  // peers' regions opened with cudaIpcOpenMemHandle
+  cudaEvent_t ev_ep_done = nullptr;  // the last EP step's completion (tide_ctx_ep_wait)
   unsigned* dst_l = nullptr;      // [El, rows_all] owner rank << 28 | pair row of each list slot (p2p)
 
   // per-phase timing (tide_ctx_set_timing)
@@ -367,10 +382,13 @@ void tide_ctx_destroy(tide_ctx* c) {
     if (p) cudaFreeHost(p);
   for (cudaEvent_t e : c->ev_chunk_ready) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_chunk_done) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->pf_ev) cudaEventDestroy(e);
+  if (c->ev_pf_free) cudaEventDestroy(c->ev_pf_free);
   for (auto& r : c->pending)
     for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  cudaEvent_t evs[] = {c->ev_route, c->ev_book, c->ev_info, c->ev_gemm1, c->ev_side_done};
+  cudaEvent_t evs[] = {c->ev_route, c->ev_book, c->ev_info, c->ev_gemm1, c->ev_side_done,
+                       c->ev_ep_done};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
@@ -492,6 +510,8 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->knob_route_one_per_sm = getenv("TIDE_ROUTE_ONE_PER_SM") != nullptr;
   c->knob_fused_combine = getenv("TIDE_FUSED_COMBINE") != nullptr;
   c->knob_route_ksplit1 = getenv("TIDE_ROUTE_KSPLIT1") != nullptr;
+  c->knob_pf_by_hits = getenv("TIDE_PF_BY_HITS") != nullptr;
+  c->knob_pf_whole = getenv("TIDE_PF_WHOLE_EXPERT") != nullptr;
   *out = c;
   return TIDE_OK;
 }
@@ -651,6 +671,52 @@ tide_status tide_ctx_ep_error(tide_ctx* c, int32_t* err) {
   return TIDE_OK;
 }
 
+tide_status tide_ctx_ep_wait(tide_ctx* c, int32_t timeout_ms) {
+  if (!c || !c->ep) return fail(TIDE_EINVAL, "not an expert-parallel context");
+  if (timeout_ms < 0) return fail(TIDE_EINVAL, "timeout_ms %d < 0", timeout_ms);
+  CU_TRY(cudaSetDevice(c->device));
+  if (!c->ev_ep_done) return TIDE_OK;  // no step yet
+  const auto t0 = std::chrono::steady_clock::now();
+  while (true) {
+    const cudaError_t q = cudaEventQuery(c->ev_ep_done);
+    if (c->comm) {
+      ncclResult_t ar = ncclSuccess;
+      NC_TRY(ncclCommGetAsyncError(c->comm, &ar));
+      if (ar != ncclSuccess && ar != ncclInProgress) {
+        if (c->own_comm) {  // a communicator shared with tide_ctx_create_ep_like contexts is
+          ncclCommAbort(c->comm);  // aborted through the context that owns it
+          c->comm = nullptr;
+        }
+        return fail(TIDE_ENCCL, "NCCL asynchronous error: %s%s", ncclGetErrorString(ar),
+                    c->own_comm ? " (communicator aborted)" : "");
+      }
+    }
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(TIDE_ECUDA, "step failed: %s", cudaGetErrorString(q));
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                        std::chrono::steady_clock::now() - t0).count();
+    if (ms > timeout_ms) {
+      if (c->comm) {
+        if (c->own_comm) {
+          ncclCommAbort(c->comm);
+          c->comm = nullptr;
+        }
+        return fail(TIDE_ENCCL, "EP step not complete after %d ms%s", timeout_ms,
+                    c->own_comm ? " (communicator aborted)" : "");
+      }
+      return fail(TIDE_ECUDA, "EP step not complete after %d ms", timeout_ms);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  if (c->p2p) {
+    int32_t err = 0;
+    tide_status s = tide_ctx_ep_error(c, &err);
+    if (s != TIDE_OK) return s;
+    if (err) return fail(TIDE_ECUDA, "a peer-memory wait timed out (a peer did not arrive)");
+  }
+  return TIDE_OK;
+}
+
 tide_status tide_ctx_create_ep_like(const tide_layer_desc* d, tide_ctx* parent, tide_ctx** out) {
   if (!parent || !parent->ep) return fail(TIDE_EINVAL, "parent is not an expert-parallel context");
   return ctx_create_ep_impl(d, parent->device, nullptr, parent, parent->rank, parent->world, out);
@@ -661,7 +727,7 @@ tide_status tide_ctx_create_ep_like(const tide_layer_desc* d, tide_ctx* parent, 
 // failed call leaves the context as it was (the next call retries).
 static tide_status ensure_pool(tide_ctx* c) {
   if (c->pool) return TIDE_OK;
-  const int slots = c->capacity + c->staging;
+  const int slots = c->capacity + c->staging + c->pf_slots_req;
   const int E = c->E;
   const int max_chunks = E + 2, max_entries2 = E + (c->maxN * c->k) / kMaxTok + 2;
   void* pool = nullptr;
@@ -702,6 +768,19 @@ static tide_status ensure_pool(tide_ctx* c) {
   for (int i = 0; ok && i < max_chunks; ++i)
     ok = cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) == cudaSuccess;
+  std::vector<cudaEvent_t> pfev(c->pf_slots_req, nullptr);
+  cudaEvent_t pf_free = nullptr;
+  for (int i = 0; ok && i < c->pf_slots_req; ++i)
+    ok = cudaEventCreateWithFlags(&pfev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (ok && c->pf_slots_req > 0) {
+    ok = cudaEventCreateWithFlags(&pf_free, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventRecord(pf_free, 0) == cudaSuccess;
+  }
+  if (!ok) {
+    for (cudaEvent_t e : pfev)
+      if (e) cudaEventDestroy(e);
+    if (pf_free) cudaEventDestroy(pf_free);
+  }
   if (ok) {
     for (int i = 0; i < E; ++i) h_slot_of[i] = -1;
     ok = cudaMemcpy(c->slot_of_dev, h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -723,7 +802,10 @@ static tide_status ensure_pool(tide_ctx* c) {
   c->max_entries2 = max_entries2;
   c->ev_chunk_ready = std::move(ready);
   c->ev_chunk_done = std::move(done);
-  c->owner.assign(slots, -1);
+  c->pf_ev = std::move(pfev);
+  c->ev_pf_free = pf_free;
+  c->pf_exp.assign(c->pf_slots_req, -1);
+  c->owner.assign(c->capacity + c->staging, -1);  // retained + staging slots (prefetch apart)
   return TIDE_OK;
 }
 
@@ -749,12 +831,19 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.pf_n = nullptr;
   p.pf_max = 0;
   p.pf_xb = 0;
+  p.pf_span = 0;
+  p.pf_shared = nullptr;
   if (prefetch && c->pf_next && c->pf_weights && c->pf_max > 0) {
     p.pf_base = static_cast<const uint8_t*>(c->pf_weights);
     p.pf_list = c->pf_next->pf_list;
     p.pf_n = c->pf_next->pf_n;
-    p.pf_max = c->pf_max;
     p.pf_xb = (long long)c->pf_next->expert_bytes;
+    // the gate/up rows only (2/3 of an expert: what the FFN's first wave of phase-1 items
+    // reads) unless TIDE_PF_WHOLE_EXPERT; the byte budget then covers more experts
+    p.pf_span = c->knob_pf_whole ? p.pf_xb : p.pf_xb / 3 * 2;
+    p.pf_max = (int)std::min<int64_t>(c->pf_next->E + 1, c->pf_budget / p.pf_span);
+    // the next layer's shared expert (known once it has run a step) goes first
+    p.pf_shared = c->knob_pf_by_hits ? nullptr : static_cast<const uint8_t*>(c->pf_next->map_shared_src);
   }
   p.slot_of = slot_of;
   p.off_out = c->off;
@@ -874,6 +963,7 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   b.par = par;
   b.pf_list = (c->pf_target && !E_override) ? c->pf_list : nullptr;
   b.pf_n = c->pf_n;
+  b.pf_by_hits = c->knob_pf_by_hits ? 1 : 0;
   b.mask = c->mask;
   b.mask_rw = c->mask;
   b.topk_idx = c->topk;
@@ -1005,6 +1095,32 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   return TIDE_OK;
 }
 
+// NEXT-3 H2D prefetch (host_master): called at the end of the previous layer's step; copies the
+// experts `n` streamed at its previous step (most-hit first, those not in HBM now) into its
+// prefetch slots on its side stream, so the link works through the gap before `n`'s own step
+// plans its copies (its route, bookkeeping and host round trip).  A wrong prediction costs
+// link time and nothing else (the slot is simply not used).
+static tide_status issue_h2d_prefetch(tide_ctx* n) {
+  if (!n->pool || !n->last_master || n->pf_exp.empty()) return TIDE_OK;
+  CU_TRY(cudaStreamWaitEvent(n->side, n->ev_pf_free, 0));  // its last step's reads are done
+  const size_t xb = n->expert_bytes;
+  uint8_t* pool = static_cast<uint8_t*>(n->pool);
+  const uint8_t* master = static_cast<const uint8_t*>(n->last_master);
+  const int base = n->capacity + n->staging;
+  int i = 0;
+  for (int e : n->last_streamed) {
+    if (i == (int)n->pf_exp.size()) break;
+    if (n->slot_of[e] >= 0) continue;  // in HBM now
+    CU_TRY(cudaMemcpyAsync(pool + (size_t)(base + i) * xb, master + (size_t)e * xb, xb,
+                           cudaMemcpyHostToDevice, n->side));
+    CU_TRY(cudaEventRecord(n->pf_ev[i], n->side));
+    n->pf_exp[i] = e;
+    ++i;
+    n->pf_issued++;
+  }
+  return TIDE_OK;
+}
+
 // host_master: plan and enqueue the H2D copies (a6) and the staged FFN chunks (a8).
 // Slot semantics (R-12/R-13): an expert in HBM at step start is served from HBM this
 // step; a slot released by an expert that is hit this step is rewritten only after the
@@ -1047,7 +1163,18 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
       slot_of[e] = -1;
     }
   }
-  struct Copy { int e, dst; bool after_gemm1, staged; };
+  // NEXT-3 H2D prefetch: experts the previous layer's step already copied into this
+  // context's prefetch slots (predicted from this layer's previous step) are not copied
+  // again: a staged one is computed from its prefetch slot, a promoted one is moved into
+  // its retained slot by a device-to-device copy
+  auto prefetched = [&](int e) -> int {
+    for (int i = 0; i < (int)c->pf_exp.size(); ++i)
+      if (c->pf_exp[i] == e) return i;
+    return -1;
+  };
+  *copies += c->pf_issued;  // H2D copies issued for this step by the previous layer
+  c->pf_issued = 0;
+  struct Copy { int e, dst; bool after_gemm1, staged; int pf; };
   std::vector<Copy> hit_copies, cold_copies;
   size_t fn = 0, fa = 0;
   auto take_slot = [&](bool& after) -> int {
@@ -1057,7 +1184,7 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   };
   for (int e = 0; e < E; ++e) {
     if (hits[e] == 0 || loaded0[e]) continue;
-    Copy cp{e, -1, false, false};
+    Copy cp{e, -1, false, false, prefetched(e)};
     if (pl[e]) {
       cp.dst = take_slot(cp.after_gemm1);
       owner[cp.dst] = e;
@@ -1070,23 +1197,29 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   if (!lazy)
     for (int e = 0; e < E; ++e)
       if (pl[e] && slot_of[e] < 0 && hits[e] == 0) {
-        Copy cp{e, -1, false, false};
+        Copy cp{e, -1, false, false, -1};
         cp.dst = take_slot(cp.after_gemm1);
         owner[cp.dst] = e;
         slot_of[e] = cp.dst;
         cold_copies.push_back(cp);
       }
   *streamed = (int)hit_copies.size();
+  // prefetched experts first (their bytes are already in flight), then the others; slots
+  // freed only after the resident FFN last (stable: ascending id within each class)
+  std::stable_partition(hit_copies.begin(), hit_copies.end(),
+                        [](const Copy& a) { return a.pf >= 0; });
   std::stable_partition(hit_copies.begin(), hit_copies.end(),
                         [](const Copy& a) { return !a.after_gemm1; });
   std::vector<std::pair<int, int>> chunks;  // [begin, end) into hit_copies
   {
     int b = 0, used = 0;
     for (int i = 0; i < (int)hit_copies.size(); ++i) {
-      const bool boundary = (hit_copies[i].staged && used == half) ||
-                            (i > b && hit_copies[i].after_gemm1 && !hit_copies[i - 1].after_gemm1);
+      const bool needs_stage = hit_copies[i].staged && hit_copies[i].pf < 0;
+      const bool boundary = (needs_stage && used == half) ||
+                            (i > b && hit_copies[i].after_gemm1 && !hit_copies[i - 1].after_gemm1) ||
+                            (i > b && hit_copies[i].pf < 0 && hit_copies[i - 1].pf >= 0);
       if (boundary) { chunks.push_back({b, i}); b = i; used = 0; }
-      if (hit_copies[i].staged) used++;
+      if (needs_stage) used++;
     }
     if (b < (int)hit_copies.size()) chunks.push_back({b, (int)hit_copies.size()});
   }
@@ -1099,7 +1232,7 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
     int stage_i = 0;
     for (int i = chunks[ci].first; i < chunks[ci].second; ++i) {
       Copy& cp = hit_copies[i];
-      if (cp.staged) cp.dst = C + (int)(ci % 2) * half + (stage_i++);
+      if (cp.staged) cp.dst = cp.pf >= 0 ? C + S + cp.pf : C + (int)(ci % 2) * half + (stage_i++);
       const int m = hits[cp.e];
       for (int t = 0; t < m; t += kMaxTok) {
         c->h_entries2[ne++] = make_int4(cp.dst, off[cp.e] + t, std::min(kMaxTok, m - t),
@@ -1128,6 +1261,13 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
         CU_TRY(cudaStreamWaitEvent(c->side, c->ev_gemm1, 0));
         waited_gemm1 = true;
       }
+      if (cp.pf >= 0) {  // already in a prefetch slot (H2D enqueued by the previous layer)
+        CU_TRY(cudaStreamWaitEvent(c->side, c->pf_ev[cp.pf], 0));
+        if (!cp.staged)  // retained: HBM-to-HBM into its slot
+          CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, pool + (size_t)(C + S + cp.pf) * xb,
+                                 xb, cudaMemcpyDeviceToDevice, c->side));
+        continue;
+      }
       CU_TRY(cudaMemcpyAsync(pool + (size_t)cp.dst * xb, master + (size_t)cp.e * xb, xb,
                              cudaMemcpyHostToDevice, c->side));
       (*copies)++;
@@ -1154,6 +1294,22 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
   CU_TRY(cudaMemcpyAsync(c->slot_of_dev, c->h_slot_of, sizeof(int) * E, cudaMemcpyHostToDevice, st));
   c->slot_of = std::move(slot_of);
   c->owner = std::move(owner);
+  // NEXT-3 H2D prefetch: the prefetch slots are free once this step's FFN launches are done;
+  // remember what streamed (hit, not in HBM), most-hit first: the prediction for the next
+  // step, which the previous layer's step prefetches into those slots
+  if (!c->pf_exp.empty()) {
+    std::fill(c->pf_exp.begin(), c->pf_exp.end(), -1);
+    CU_TRY(cudaEventRecord(c->ev_pf_free, st));
+    c->last_streamed.clear();
+    for (const Copy& cp : hit_copies) c->last_streamed.push_back(cp.e);
+    std::stable_sort(c->last_streamed.begin(), c->last_streamed.end(),
+                     [hits](int a, int b) { return hits[a] > hits[b]; });
+    c->last_master = master;
+  }
+  if (c->pf_next_h) {
+    tide_status s = issue_h2d_prefetch(c->pf_next_h);
+    if (s != TIDE_OK) return s;
+  }
   return TIDE_OK;
 }
 
@@ -1192,7 +1348,7 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   const int E = c->E, k = c->k, H = c->H;
   const int refresh = (step % interval) == 0;
   tide_status s = ensure_weight_maps(c, pool_mode ? c->pool : w->device_all,
-                                     pool_mode ? c->capacity + c->staging : E,
+                                     pool_mode ? c->capacity + c->staging + c->pf_slots_req : E,
                                      shared ? w->shared_w : nullptr);
   if (s != TIDE_OK) return s;
 
@@ -1263,13 +1419,13 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     if (c->bf16)
       CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
-                        (const int*)c->pair_slot, (const int*)c->off,
+                        (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
                         static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr));
     else
       CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), 0, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
-                        (const int*)c->pair_slot, (const int*)c->off, static_cast<float*>(out),
-                        N, k, H, shared ? 1 : 0, ctr));
+                        (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
+                        static_cast<float*>(out), N, k, H, shared ? 1 : 0, ctr));
     c->launches++;
   }
   if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4/a5 outputs
@@ -1430,6 +1586,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
   }
   CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // placement_out / info valid with the stream
+  if (!c->ev_ep_done) CU_TRY(cudaEventCreateWithFlags(&c->ev_ep_done, cudaEventDisableTiming));
+  CU_TRY(cudaEventRecord(c->ev_ep_done, st));  // tide_ctx_ep_wait
   if (c->timing) {
     CU_TRY(cudaEventRecord(rec.ev[6], st));
     rec.launches = c->launches - launches0;
@@ -1578,16 +1736,29 @@ tide_status tide_ctx_set_prefetch(tide_ctx* c, tide_ctx* next, const void* next_
   if (budget_bytes < 0) return fail(TIDE_EINVAL, "budget_bytes %lld < 0", (long long)budget_bytes);
   if (next && next->device != c->device)
     return fail(TIDE_EINVAL, "next context is on device %d, this one on %d", next->device, c->device);
-  if (next && !next_device_all) return fail(TIDE_EINVAL, "next_device_all is null");
-  if (!next || budget_bytes == 0) {
+  if (next && !next_device_all) {  // host_master: H2D prefetch into `next`'s prefetch slots
+    if (next->pool && next->pf_slots_req == 0)
+      return fail(TIDE_EINVAL, "H2D prefetch for a context that already ran a host_master step");
+    if (!next->pool)
+      next->pf_slots_req = (int)std::min<int64_t>(std::min(next->E, 64),
+                                                  budget_bytes / (int64_t)next->expert_bytes);
+    c->pf_next_h = next->pf_slots_req > 0 ? next : nullptr;
     c->pf_next = nullptr;
     c->pf_weights = nullptr;
     c->pf_max = 0;
     return TIDE_OK;
   }
+  if (!next || budget_bytes == 0) {
+    c->pf_next = nullptr;
+    c->pf_weights = nullptr;
+    c->pf_max = 0;
+    c->pf_next_h = nullptr;
+    return TIDE_OK;
+  }
   c->pf_next = next;
   c->pf_weights = next_device_all;
   c->pf_max = (int)std::min<int64_t>(next->E, budget_bytes / (int64_t)next->expert_bytes);
+  c->pf_budget = budget_bytes;
   next->pf_target = true;
   return TIDE_OK;
 }

@@ -32,7 +32,7 @@ EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert
             "tide_ctx_create_ep", "tide_ctx_create_ep_like", "tide_moe_step_ep",
             "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats",
             "tide_ctx_create_ep_p2p", "tide_ep_handle_bytes", "tide_ctx_ep_export",
-            "tide_ctx_ep_connect", "tide_ctx_ep_error", "tide_interval_profile",
+            "tide_ctx_ep_connect", "tide_ctx_ep_error", "tide_ctx_ep_wait", "tide_interval_profile",
             "tide_interval_cost_trace", "tide_optimize_interval_trace")
 
 
@@ -149,6 +149,7 @@ def lib():
                                          ctypes.POINTER(ctypes.c_void_p)]
         L.tide_ctx_ep_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.tide_ctx_ep_error.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
+        L.tide_ctx_ep_wait.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.tide_interval_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
         L.tide_interval_cost_trace.argtypes = [ctypes.POINTER(IntervalTraceModel), ctypes.c_int32,
@@ -248,7 +249,9 @@ class Context:
     def set_prefetch(self, next_ctx: "Context | None", next_device_all=None,
                      budget_bytes: int = 0):
         """tide_ctx_set_prefetch: prefetch `next_ctx`'s likely experts into L2 at the end of
-        this context's FFN (NEXT-3); None / 0 disables."""
+        this context's FFN (NEXT-3; next_device_all = its packed experts), or, with
+        next_device_all None (next serves from a pinned host master), copy its predicted
+        streamed experts host-to-HBM into its prefetch slots; None / 0 disables."""
         _check(lib().tide_ctx_set_prefetch(
             self.handle, next_ctx.handle if next_ctx is not None else None,
             _ptr(next_device_all) if next_device_all is not None else None, int(budget_bytes)))
@@ -344,6 +347,12 @@ class EPContext(Context):
         self.local_experts = desc.num_experts // world
         self.capacity = self.local_experts
         self.device = device
+
+    def wait(self, timeout_ms: int = 20000):
+        """tide_ctx_ep_wait: host wait for the last step with NCCL async-error polling; raises
+        TideError (TIDE_ENCCL / TIDE_ECUDA) on a communicator error, a peer-memory wait that
+        gave up, or a timeout."""
+        _check(lib().tide_ctx_ep_wait(self.handle, int(timeout_ms)))
 
     def moe_step_ep(self, block_hidden, router_w, local_experts, *, shared_w=None, placement,
                     step: int, interval: int, capacity: int | None = None, out=None,

@@ -104,3 +104,22 @@ def test_ep_world2():
     for rank, err, hits_ok in res:
         assert not isinstance(err, str), err
         assert hits_ok and err < OUT_TOL, (rank, err)
+
+
+def test_ep_wait_reports_completion():
+    """tide_ctx_ep_wait (failure handling): returns once the last EP step completed, for the
+    NCCL exchange (with ncclCommGetAsyncError polling) and the peer-memory exchange."""
+    from paper_2605_20179_b200 import tide
+    shape = g.Shape("epw", 32, 4, 256, 256, 1, 16, steps=2, dtype="bf16", shared_expert=True)
+    layer = DeviceLayer(shape, 81)
+    desc = desc_for(shape)
+    nccl = tide.EPContext(desc, tide.nccl_unique_id(), 0, 1)
+    p2p = tide.EPPeerContext(desc, 0, 1)
+    p2p.connect(bases=[p2p.export()[1]])
+    x = g.np_to_torch(g.block_hidden_np(shape, 81)[0], "cuda")
+    for ctx in (nccl, p2p):
+        ctx.wait(1000)  # no step yet: returns at once
+        ctx.moe_step_ep(x, layer.router, layer.device_all, shared_w=layer.shared,
+                        placement=torch.zeros(32, dtype=torch.uint8, device="cuda"), step=0,
+                        interval=1)
+        ctx.wait(20000)

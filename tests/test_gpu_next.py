@@ -83,3 +83,39 @@ def test_counter_modes_schedule(counter, incumbent):
             assert (r.placement.cpu().numpy() == want).all(), (blk, t)
             assert torch.equal(r.out.view(torch.int16), r0.out.view(torch.int16))
             p = want
+
+
+def test_h2d_prefetch_is_bitwise_neutral_and_used():
+    """NEXT-3 H2D prefetch (host_master): a 3-layer ring at C < E where each layer's step
+    copies the next layer's predicted streamed experts into that layer's prefetch slots.
+    Outputs, hits and placements are bitwise those of the same ring without prefetch; the
+    prefetched experts are used (fewer H2D copies on the steps after the first), and every
+    prefetch copy is counted in the stats."""
+    from paper_2605_20179_b200 import tide
+    shape = g.Shape("pfh", 32, 4, 256, 256, 1, 24, steps=6, dtype="bf16", shared_expert=True)
+    E, C = shape.num_experts, 6
+    layers = [DeviceLayer(shape, 90 + l, host_master=True) for l in range(3)]
+    xs = [g.block_hidden_np(shape, 90 + l) for l in range(3)]
+
+    def run(prefetch):
+        ctxs = [tide.Context(desc_for(shape), C, 4) for _ in layers]
+        if prefetch:
+            for l, c in enumerate(ctxs):
+                c.set_prefetch(ctxs[(l + 1) % 3], None, 4 * shape.expert_bytes)
+        pls = [torch.zeros(E, dtype=torch.uint8, device="cuda") for _ in layers]
+        res, copies = [], 0
+        for t in range(shape.steps):
+            for l, (L, c) in enumerate(zip(layers, ctxs)):
+                r = c.moe_step(g.np_to_torch(xs[l][t], "cuda"), L.router, **L.weights("host_master"),
+                               placement=pls[l], step=t, interval=2, placement_out=pls[l], stats=True)
+                torch.cuda.synchronize()
+                res.append((r.out.view(torch.int16).cpu().numpy().copy(),
+                            r.hit_counts.cpu().numpy().copy(), r.placement.cpu().numpy().copy()))
+                copies += r.stats["copies"]
+        return res, copies
+
+    base, c0 = run(False)
+    got, c1 = run(True)
+    for (a, ha, pa), (b, hb, pb) in zip(base, got):
+        assert (a == b).all() and (ha == hb).all() and (pa == pb).all()
+    assert c1 > 0 and c0 > 0
