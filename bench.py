@@ -229,6 +229,7 @@ def _cpu_model() -> str:
 def h2d_peak_gbs(dev, mb: int = 256, reps: int = 5) -> float:
     """Pinned-host -> HBM copy bandwidth (best of `reps` copies of `mb` MB, CUDA events):
     the PCIe roofline for the pinned-host serving path (a6, SURVEY 8(d) metric 4)."""
+    torch.cuda.synchronize()  # no copy of the run (e.g. an H2D prefetch) shares the link
     src = torch.empty(mb << 20, dtype=torch.uint8).pin_memory()
     dst = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

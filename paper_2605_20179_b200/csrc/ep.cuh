@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
 //                           the token count go straight into every rank's x_all /
 //                           topk_all / gates_all / ntok at [rank*maxN + n]; one arrival per
 //                           source rank on each destination's dispatch counter
-//   tide_ep_lists_kernel    (p2p) waits until all P sources have arrived
+//                           the route grid's last CTA then waits until all P sources have
+//                           arrived and builds the local experts' token lists (route_ep_lists)
 //   tide_ffn_kernel<T,true> (p2p) the phase-2 epilogue stores each routed pair's y row
 //                           straight into the owning rank's ypair[n*k + j]; the grid's last
 //                           CTA delivers the local experts' counts into every hits_all and
@@ -124,9 +125,9 @@ __global__ void __launch_bounds__(128) tide_ep_final_kernel(const float* __restr
 //   tide_ep_final_kernel    (p2p) waits for the P arrivals, then exactly the single-device
 //                           combine: out[n] = sum_j g[n,j] y[n,j] in slot order (+ shared),
 //                           so the EP output equals the single-device output bit for bit
-// Counters are double-buffered by the step parity word the route kernel flips; the lists
-// kernel of a step zeroes the other parity's counters (their last readers finished a step
-// ago; their next writers need this step's partials first).  A waiting CTA gives up after
+// Counters are double-buffered by the step parity word the route kernel flips; the route's
+// list build of a step zeroes the other parity's counters (their last readers finished a
+// step ago; their next writers need this step's partials first).  A waiting CTA gives up after
 // kEpWaitNs, records the failure in the context's error word and returns (no GPU hang).
 constexpr int kEpMaxWorld = 8;
 constexpr unsigned long long kEpWaitNs = 20000000000ull;  // 20 s
@@ -174,38 +175,6 @@ __device__ __forceinline__ bool ep_wait_all(const unsigned* ctr, unsigned target
   }
   __syncthreads();
   return s_ok != 0;
-}
-
-// p2p variant of tide_ep_lists_kernel: wait for the P sources' dispatch first; rows past a
-// source's token count hold stale routing and are skipped (pslot -1).
-__global__ void __launch_bounds__(256) tide_ep_lists_p2p_kernel(
-    char* sym, EpSymLayout lay, const int* par_word, unsigned target, int rows, int maxN, int k,
-    int e0, int El, int* __restrict__ cnt_l, int* __restrict__ list_l, int list_stride,
-    int* __restrict__ pslot_all, unsigned* __restrict__ dst_l) {
-  pdl_wait();  // this rank's route kernel (and its cnt_l zeroing) is complete
-  unsigned* ctr = reinterpret_cast<unsigned*>(sym + lay.ctr);
-  const int par = __ldcg(par_word);
-  if (!ep_wait_all(ctr + par, target, ctr + 4)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // other parity: free for the next step
-    ctr[par ^ 1] = 0u;
-    ctr[2 + (par ^ 1)] = 0u;
-  }
-  const int* topk_all = reinterpret_cast<const int*>(sym + lay.topk_all);
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= rows * k) return;
-  const int row = q / k, src = row / maxN;
-  const bool live = row - src * maxN < __ldcg(reinterpret_cast<const int*>(sym + lay.ntok) + src);
-  const int e = live ? __ldcg(topk_all + q) : -1;
-  if (e >= e0 && e < e0 + El) {
-    const int s = atomicAdd(&cnt_l[e - e0], 1);
-    list_l[(size_t)(e - e0) * list_stride + s] = q / k;
-    // where the FFN epilogue stores this pair's y: source rank << 28 | its row n*k + j there
-    dst_l[(size_t)(e - e0) * list_stride + s] =
-        ((unsigned)src << 28) | (unsigned)((row - src * maxN) * k + (q - row * k));
-    pslot_all[q] = s;
-  } else {
-    pslot_all[q] = -1;
-  }
 }
 
 // p2p variant of tide_ep_final_kernel: grid (max(N,1), ceil(H/512)), 128 threads x 4 columns.

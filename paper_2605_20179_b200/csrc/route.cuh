@@ -101,6 +101,12 @@ struct RouteParams {
   size_t ep_off_x, ep_off_topk, ep_off_gates, ep_off_ntok, ep_off_ctr;
   int* zero_j;                 // EP: local-expert counts zeroed by CTA (0,0)
   int n_zero_j;
+  // peer-memory EP: the grid's last CTA builds the local experts' lists (route_ep_lists)
+  int ep_lists, ep_e0, ep_El, ep_rows;  // rows = P * maxN
+  int* ep_cnt_l;               // [El] counts over every rank's rows (zeroed via zero_j)
+  int* ep_list_l;              // [El][rows] x_all row of each list slot
+  int* ep_pslot;               // [rows * k] slot of each pair (-1: not a local expert)
+  unsigned* ep_dst_l;          // [El][rows] owner rank << 28 | pair row of each list slot
 };
 
 struct BookParams {
@@ -272,6 +278,63 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
     }
 }
 
+// Peer-memory EP, in the route grid's last CTA (after its dispatch arrivals): wait until all
+// P sources have dispatched this step (own included), then build the local experts' token
+// lists over every rank's rows -- counts, lists, per-pair slots and the destination of each
+// list slot's y row (owner rank << 28 | its pair row there) -- for the FFN that follows; rows
+// past a source's token count hold stale routing and are skipped.  It also frees the other
+// parity's dispatch / combine counters for the next step (their last readers are done).
+// A wait that gives up after 20 s records the failure in the error word and returns.
+__device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, int& s_last) {
+  __syncthreads();  // s_last was set by thread 0
+  if (!s_last) return;
+  char* sym = p.ep_base[p.ep_rank];
+  unsigned* ctr = reinterpret_cast<unsigned*>(sym + p.ep_off_ctr);
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    const unsigned* cw = ctr + (par ^ 1);
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cw) : "memory");
+    if (v < (unsigned)p.ep_P) {
+      const unsigned long long t0 = globaltimer_ns();
+      do {
+        __nanosleep(64);
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cw) : "memory");
+        if (globaltimer_ns() - t0 > 20000000000ull) {
+          atomicExch(ctr + 4, 1u);
+          ok = 0;
+          break;
+        }
+      } while (v < (unsigned)p.ep_P);
+    }
+    if (ok) {
+      ctr[par] = 0u;
+      ctr[2 + par] = 0u;
+    }
+    s_last = ok;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const int k = p.k, maxN = p.maxN, e0 = p.ep_e0, El = p.ep_El;
+  const int* topk_all = reinterpret_cast<const int*>(sym + p.ep_off_topk);
+  const int* ntok = reinterpret_cast<const int*>(sym + p.ep_off_ntok);
+  for (int q = threadIdx.x; q < p.ep_rows * k; q += blockDim.x) {
+    const int row = q / k, src = row / maxN;
+    const bool live = row - src * maxN < __ldcg(ntok + src);
+    const int e = live ? __ldcg(topk_all + q) : -1;
+    if (e >= e0 && e < e0 + El) {
+      const int s = atomicAdd(&p.ep_cnt_l[e - e0], 1);
+      p.ep_list_l[(size_t)(e - e0) * p.ep_rows + s] = row;
+      p.ep_dst_l[(size_t)(e - e0) * p.ep_rows + s] =
+          ((unsigned)src << 28) | (unsigned)((row - src * maxN) * k + (q - row * k));
+      p.ep_pslot[q] = s;
+    } else {
+      p.ep_pslot[q] = -1;
+    }
+  }
+  pdl_trigger();  // the grid's other CTAs have exited: the FFN may launch now
+}
+
 // Shared tail of both route kernels: arrive on the token group's counter; the group's last
 // CTA runs phase 2 (top-k a2, histogram + token lists a3) for its tokens; the last phase-2
 // CTA of the grid flips the count parity (all CTAs have read it by then).
@@ -354,6 +417,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     if (tr) tr[3] = globaltimer_ns();
     // every CTA has read par; EP: system-scope release of this CTA's peer top-k / gate stores
     const int old = p.ep_P > 1 ? atom_add_acq_rel_sys(p.g_done, 1) : atom_add_acq_rel_gpu(p.g_done, 1);
+    s_flag = old == (int)gridDim.y - 1;  // the grid's last CTA
     if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
@@ -368,6 +432,7 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
       }
     }
   }
+  if (p.ep_lists) route_ep_lists(p, par, s_flag);
 }
 
 // Peer-memory EP dispatch of X: CTA (bx, by) stores uint4 columns [bx*per, (bx+1)*per) of
@@ -396,7 +461,9 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   const int E = p.E, N = p.N, H = p.H;
   const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
   pdl_wait();     // X may be written by the previous kernel in the stream
-  pdl_trigger();  // let the FFN grid start its prologue
+  // let the FFN grid start its prologue; peer-memory EP: only once the local lists exist
+  // (route_ep_lists), so a resident FFN never holds SMs a waited-on peer still needs
+  if (!p.ep_lists) pdl_trigger();
   unsigned long long* tr =
       p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }
@@ -488,7 +555,7 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   const int S = p.ksplit, ks = blockIdx.x % S;  // this CTA's slice of H (S slices per tile)
   const int n0 = blockIdx.y * 8, n1 = min(N, n0 + 8), e0 = (blockIdx.x / S) * 16;
   pdl_wait();
-  pdl_trigger();
+  if (!p.ep_lists) pdl_trigger();  // see tide_route_kernel
   unsigned long long* tr =
       p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }

@@ -140,6 +140,8 @@ struct tide_ctx {
   std::vector<int> last_streamed;      // experts streamed at the last step, most-hit first
   const void* last_master = nullptr;   // the host master of the last step
   int pf_issued = 0;                   // H2D copies issued for this context's next step
+  int pf_min_hits = 2;                 // predict experts streamed with >= this many hits
+                                       // (TIDE_H2D_PF_MIN_HITS)
   int* list = nullptr;       // [E * maxN] per-expert token lists
   unsigned* mask = nullptr;  // [E * NWmax] per-expert token bitmasks
   int* g_cnt = nullptr;      // [maxN + 2] route-kernel last-CTA counters
@@ -305,7 +307,6 @@ static void preload_ep_p2p_kernels(const tide_ctx* c) {
   }
 #undef TOUCH_ROUTE
   touch(tide_book_kernel);
-  touch(tide_ep_lists_p2p_kernel);
 }
 
 extern "C" {
@@ -512,6 +513,7 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->knob_route_ksplit1 = getenv("TIDE_ROUTE_KSPLIT1") != nullptr;
   c->knob_pf_by_hits = getenv("TIDE_PF_BY_HITS") != nullptr;
   c->knob_pf_whole = getenv("TIDE_PF_WHOLE_EXPERT") != nullptr;
+  if (const char* v = getenv("TIDE_H2D_PF_MIN_HITS")) c->pf_min_hits = std::max(1, atoi(v));
   *out = c;
   return TIDE_OK;
 }
@@ -1026,6 +1028,7 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.ep_rank = 0;
   rp.zero_j = nullptr;
   rp.n_zero_j = 0;
+  rp.ep_lists = 0;
   if (c->p2p) {  // peer-memory EP: the router dispatches (route.cuh)
     rp.ep_P = c->world;
     rp.ep_rank = c->rank;
@@ -1037,6 +1040,14 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
     rp.ep_off_ctr = c->lay.ctr;
     rp.zero_j = c->cnt_l;
     rp.n_zero_j = c->El;
+    rp.ep_lists = 1;  // the local experts' lists are built by the route grid's last CTA
+    rp.ep_e0 = c->e0;
+    rp.ep_El = c->El;
+    rp.ep_rows = c->rows_all;
+    rp.ep_cnt_l = c->cnt_l;
+    rp.ep_list_l = c->list_l;
+    rp.ep_pslot = c->pslot_all;
+    rp.ep_dst_l = c->dst_l;
   }
   // bf16 routers run phase 1 on the tensor cores (16 experts x 8 tokens per CTA);
   // TIDE_ROUTER_CC=1 forces the CUDA-core kernel (A/B measurement)
@@ -1301,7 +1312,8 @@ static tide_status pool_step(tide_ctx* c, const tide_expert_weights* w, const Ro
     std::fill(c->pf_exp.begin(), c->pf_exp.end(), -1);
     CU_TRY(cudaEventRecord(c->ev_pf_free, st));
     c->last_streamed.clear();
-    for (const Copy& cp : hit_copies) c->last_streamed.push_back(cp.e);
+    for (const Copy& cp : hit_copies)  // experts hit by a single token flicker: not predicted
+      if (hits[cp.e] >= c->pf_min_hits) c->last_streamed.push_back(cp.e);
     std::stable_sort(c->last_streamed.begin(), c->last_streamed.end(),
                      [hits](int a, int b) { return hits[a] > hits[b]; });
     c->last_master = master;
@@ -1523,17 +1535,15 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[2], st));
   // local experts' token lists over all rows; their counts are the global hits (R-18)
-  if (c->p2p) {  // cnt_l was zeroed by the route kernel
-    CU_TRY(launch_pdl(tide_ep_lists_p2p_kernel, dim3((R * k + 255) / 256), dim3(256), 0, st,
-                      c->sym, c->lay, (const int*)c->cnt_par, (unsigned)c->world, R, maxN, k,
-                      c->e0, El, c->cnt_l, c->list_l, R, c->pslot_all, c->dst_l));
+  if (c->p2p) {
+    // built by the route grid's last CTA once every rank dispatched (route_ep_lists)
   } else {
     CU_TRY(cudaMemsetAsync(c->cnt_l, 0, sizeof(int) * El, st));
     tide_ep_lists_kernel<<<(R * k + 255) / 256, 256, 0, st>>>(c->topk_all, R, k, c->e0, El,
                                                             c->cnt_l, c->list_l, R, c->pslot_all);
     CU_TRY(cudaGetLastError());
+    c->launches++;
   }
-  c->launches++;
   // a4: placement of the local experts runs beside the FFN on the side stream (the FFN
   // computes every hit local expert; placement' only drives I/O), joined before the end
   CU_TRY(cudaEventRecord(c->ev_route, st));
