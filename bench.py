@@ -732,6 +732,9 @@ def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full
     cap = min(args.capacity or El, El)
     st = Stack(args, s, dev, rank, world, cap, "ep", weights=weights, p2p=p2p)
     steps, warmup = args.steps, args.warmup
+    pf_mb = args.prefetch_mb if args.prefetch_mb >= 0 else 32.0  # next layer's local experts
+    if pf_mb > 0:
+        st.set_prefetch(pf_mb)
     for i in range(warmup):
         st.step(i)
     torch.cuda.synchronize()
@@ -789,6 +792,7 @@ def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full
                        else "NCCL collectives",
            "launch": "CUDA graph per block step (all layers), replayed" if graphs
                      else "eager stream",
+           "prefetch_mb": pf_mb,
            "gpu_launches": launches,
            "roofline": {"bound": "hbm", "achieved": round(ach_min, 1), "peak": peak,
                         "unit": "GB/s", "frac": round(ach_min / peak, 4), "traffic": None,

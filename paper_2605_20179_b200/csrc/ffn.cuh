@@ -33,9 +33,7 @@ constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 
 constexpr int kStageBytes = 2 * kATile + kBTile;
 constexpr int kPfPiece = 64 * 1024;  // bytes per L2 bulk prefetch
 constexpr int kMaxEntriesSmem = 1280;          // work entries built per CTA (E + N*k/128 + ...)
-constexpr int kMaxExpertsSmem = 1024;          // row offset of every expert (fused combine)
-constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem +
-                              4 * kMaxExpertsSmem;
+constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem;
 
 struct FfnParams {
   CUtensorMap map_gu;    // routed pool viewed as rows of H elements (gate/up rows)
@@ -85,68 +83,12 @@ struct FfnParams {
   size_t ep_off_ypair, ep_off_hits, ep_off_ctr;
   int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
   int shared_tok0;       // token id of its first row (0 single-device, rank*maxN under EP)
-  // a10 combine fused into the phase-2 epilogue (single device, build mode; cmb_out == nullptr:
-  // the separate tide_combine_kernel runs).  Every (token n, H-tile) slice of y is complete
-  // after k (+ shared) phase-2 items, one per routed pair (and the shared expert's), each
-  // arriving (acq_rel) on the slice's counter once its y rows are stored; the CTA that brings
-  // the count to k (+1) computes out[n, tile] = sum_j g[n,j] y[row(n,j), tile] (+ y_shared) in
-  // slot order with the combine kernel's exact arithmetic (fp32 FMA chain, one rounding).
-  void* cmb_out;          // [N, H] the layer's output (T)
-  int* cmb_cnt;           // [N * HT] arrival counters, zeroed by the route kernel
-  const int* cmb_topk;    // [N, k]
-  const int* cmb_slot;    // [N, k] slot of pair (n, j) in its expert's token list
-  const float* cmb_gates; // [N, k]
 };
 
 struct FfnItem {
   int kind;  // 0 gate/up, 1 down, -1 end
   int tile, slot, off, m, flags, entry, tokbase;
 };
-
-// a10 fused into a phase-2 epilogue (FfnParams::cmb_out), run by the 128 epilogue threads
-// right after they stored the item's y rows; `col` = this thread's column in the H-tile.
-// Arrival: thread q < m takes row q's token and arrives (acq_rel: releases this CTA's y rows
-// through the named barrier, acquires the other contributors'); the last contributor of a
-// (token, tile) slice computes it.  The arithmetic is tide_combine_kernel's, element for
-// element: acc = fma(g_j, y_j, acc) for j = 0..k-1 from 0, + y_shared, one rounding.
-template <typename T>
-__device__ __forceinline__ void fused_combine(const FfnParams& p, const FfnItem& item, int col,
-                                              const int* s_off, int* s_cmb) {
-  const int q = col, lane = threadIdx.x & 31, k = p.k, H = p.H;
-  const int HT = (H + kTileM - 1) / kTileM;
-  const int need = k + (p.shared ? 1 : 0);
-  named_bar_sync(2, 128);  // the item's y rows are stored by all 128 threads
-  if (q < item.m) {
-    const int n = (item.flags & 2) ? item.tokbase + q - p.shared_tok0
-                                   : __ldcg(p.list + item.tokbase + q);
-    const int old = atom_add_acq_rel_gpu(p.cmb_cnt + (size_t)n * HT + item.tile, 1);
-    s_cmb[q] = old == need - 1 ? n : -1;
-  }
-  named_bar_sync(2, 128);
-  const int h = item.tile * kTileM + col;
-  for (int i = 0; i < item.m; ++i) {
-    const int n = s_cmb[i];  // the same in every thread
-    if (n < 0) continue;
-    int r_j = 0;
-    float g_j = 0.f;
-    if (lane < k) {
-      const int qq = n * k + lane;
-      r_j = s_off[__ldcg(p.cmb_topk + qq)] + __ldcg(p.cmb_slot + qq);
-      g_j = __ldcg(p.cmb_gates + qq);
-    }
-    const int hh = h < H ? h : 0;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int j = 0; j < k; ++j) {
-      const int r = __shfl_sync(0xffffffffu, r_j, j);
-      const float g = __shfl_sync(0xffffffffu, g_j, j);
-      acc = fmaf(g, __ldcg(p.y_out + (size_t)r * H + hh), acc);
-    }
-    if (p.shared) acc += __ldcg(p.y_out + (size_t)(p.shared_row0 + n) * H + hh);
-    if (h < H) static_cast<T*>(p.cmb_out)[(size_t)n * H + h] = from_f32<T>(acc);
-  }
-  named_bar_sync(2, 128);  // s_cmb is rewritten by the next item
-}
 
 template <typename T, bool EP>
 __global__ void __launch_bounds__(kFfnThreads, 1)
@@ -171,7 +113,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(items + kItemSlots);
   int* s_tok = reinterpret_cast<int*>(tmem_slot + 4);  // producer: row ids of the current item
   int4* s_ent = reinterpret_cast<int4*>(s_tok + kMaxTok);  // build mode: this CTA's work list
-  int* s_off = reinterpret_cast<int*>(s_ent + kMaxEntriesSmem);  // build mode: off[e] per expert
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long* tr = p.trace ? p.trace + 8 * blockIdx.x : nullptr;
@@ -214,7 +155,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   // expert's entries in s_ent and (CTA 0) its first FFN row in off_out.
   __shared__ int s_wsum[2][kFfnThreads / 32];
   __shared__ int s_nent;
-  __shared__ int s_cmb[kMaxTok];  // fused combine: token whose slice this item completes, or -1
   if (p.cnt) {
     const int E = p.E, t = threadIdx.x;
     constexpr int PER = 4;  // experts per thread in the batched path (E <= 4 * 192)
@@ -267,7 +207,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         const int e = e0 + i, m = m4[i];
         if (e < e1) {
           if (blockIdx.x == 0) p.off_out[e] = row;
-          s_off[e] = row;
           if (m > 0 && s4[i] >= 0)
             for (int c = 0; c * kMaxTok < m; ++c)
               s_ent[ei++] = make_int4(s4[i], row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
@@ -281,7 +220,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
         const int m = __ldcg(cnt + e);
         const int slot = p.slot_of ? __ldcg(p.slot_of + e) : e;
         if (blockIdx.x == 0) p.off_out[e] = row;
-        if (e < kMaxExpertsSmem) s_off[e] = row;
         if (m > 0 && slot >= 0)
           for (int c = 0; c * kMaxTok < m; ++c)
             s_ent[ei++] = make_int4(slot, row + c * kMaxTok, min(kMaxTok, m - c * kMaxTok),
@@ -570,7 +508,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
               if (c0 + i < item.m) ycol[(size_t)(item.off + c0 + i) * H] = v[i];
           }
         }
-        if (!EP && p.cmb_out) fused_combine<T>(p, item, row, s_off, s_cmb);
       }
       tc_fence_before();
       __syncwarp();

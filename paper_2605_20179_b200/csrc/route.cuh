@@ -88,8 +88,6 @@ struct RouteParams {
   int* g_cnt;           // [gridDim.y] completion counters (self-resetting)
   int* zero_i;          // FFN scheduler counters zeroed by CTA (0,0)
   int n_zero;
-  int* zero_c;          // fused-combine counters zeroed by the whole grid
-  int n_zero_c;
   unsigned long long* trace;  // debug: 8 timestamps per CTA (nullable)
   // Peer-memory EP dispatch fused into the router (tide_ctx_create_ep_p2p; ep_P == 0: off).
   // Every CTA stores its slice of its token rows of X into every rank's x_all; each token
@@ -474,10 +472,6 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
     for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
   }
-  {  // the fused combine's (token, H-tile) counters, spread over the grid
-    const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
-    for (int i = cta * blockDim.x + tid; i < p.n_zero_c; i += ncta * blockDim.x) p.zero_c[i] = 0;
-  }
 
   // ================= phase 1: router logits (a1)
   {
@@ -565,10 +559,6 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
     for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
     for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
-  }
-  {  // the fused combine's (token, H-tile) counters, spread over the grid
-    const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
-    for (int i = cta * blockDim.x + tid; i < p.n_zero_c; i += ncta * blockDim.x) p.zero_c[i] = 0;
   }
   // ================= phase 1: router logits (a1)
   {
@@ -787,7 +777,7 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            T* __restrict__ out, int N, int k,
                                                            int H, int shared,
                                                            unsigned long long* trace) {
-  __shared__ int s_off[1024];
+  extern __shared__ int s_off[];  // [E] (dynamic: the CTA must fit beside a resident FFN CTA)
   __shared__ int s_scratch[33];
   const int n = blockIdx.x, lane = threadIdx.x & 31;
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;

@@ -152,13 +152,12 @@ struct tide_ctx {
   void* x_in = nullptr;      // [maxN, H] copy of the block's hidden states (gather4 source)
   void* h_perm = nullptr;    // [max_rows, F]
   float* y_perm = nullptr;   // [max_rows, H]
-  int* cmb_cnt = nullptr;    // [maxN * ceil(H/128)] fused-combine arrival counters
   // A/B measurement knobs, read once from the environment at context creation:
   // TIDE_ROUTE_TPC (tokens per CUDA-core router CTA), TIDE_ROUTER_CC=1 (CUDA-core router for
-  // bf16), TIDE_ROUTE_ONE_PER_SM=1 (one router CTA per SM), TIDE_FUSED_COMBINE=1 (a10 in
-  // the FFN's phase-2 epilogue instead of the combine kernel: experimental, DESIGN 11)
+  // bf16), TIDE_ROUTE_ONE_PER_SM=1 (one router CTA per SM), (see DESIGN 11
+  // for the measured negative results that removed other knobs)
   int knob_route_tpc = 0;
-  bool knob_router_cc = false, knob_route_one_per_sm = false, knob_fused_combine = false;
+  bool knob_router_cc = false, knob_route_one_per_sm = false;
   bool knob_route_ksplit1 = false;  // TIDE_ROUTE_KSPLIT1=1: one router CTA per 16 x 8 tile
   bool knob_pf_by_hits = false;    // TIDE_PF_BY_HITS=1: prefetch ranked by hits, no shared expert
   bool knob_pf_whole = false;      // TIDE_PF_WHOLE_EXPERT=1: prefetch whole experts (not gate/up)
@@ -373,7 +372,7 @@ void tide_ctx_destroy(tide_ctx* c) {
                  c->x_in,   c->h_perm,   c->y_perm,  c->ffn_ctrl,  c->info,   c->slot_of_dev,
                  c->pool,   c->entries2, c->ctrl2,   c->done2,  c->x_all,  c->topk_all,
                  c->gates_all, c->pslot_all, c->cnt_l, c->list_l, c->off_l, c->hits_l,
-                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n, c->cmb_cnt,
+                 c->partial, c->recv, c->counter_acc, c->cnt_par, c->pf_list, c->pf_n,
                  c->logits64,
                  c->dst_l};
   for (void* p : dev)
@@ -467,7 +466,6 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   ALLOC(c->h_perm, c->eb * (size_t)c->max_rows * c->F);
   ALLOC(c->y_perm, sizeof(float) * (size_t)c->max_rows * c->H);
   ALLOC(c->ffn_ctrl, sizeof(int) * (2 + c->max_entries));
-  ALLOC(c->cmb_cnt, sizeof(int) * (size_t)N * ((c->H + kTileM - 1) / kTileM));
   c->info_bytes = sizeof(RouteInfo) + sizeof(int) * E + E;
   ALLOC(c->info, c->info_bytes);
   ALLOC(c->slot_of_dev, sizeof(int) * E);
@@ -509,7 +507,6 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   if (const char* v = getenv("TIDE_ROUTE_TPC")) c->knob_route_tpc = std::max(1, std::min(8, atoi(v)));
   c->knob_router_cc = getenv("TIDE_ROUTER_CC") != nullptr;
   c->knob_route_one_per_sm = getenv("TIDE_ROUTE_ONE_PER_SM") != nullptr;
-  c->knob_fused_combine = getenv("TIDE_FUSED_COMBINE") != nullptr;
   c->knob_route_ksplit1 = getenv("TIDE_ROUTE_KSPLIT1") != nullptr;
   c->knob_pf_by_hits = getenv("TIDE_PF_BY_HITS") != nullptr;
   c->knob_pf_whole = getenv("TIDE_PF_WHOLE_EXPERT") != nullptr;
@@ -817,8 +814,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
                               const int4* entries, const int* n_entries, int* sched, int* done,
                               int N, cudaStream_t st, bool ep_local = false,
                               unsigned long long* trace = nullptr, const int* par = nullptr,
-                              bool prefetch = false, unsigned long long* itrace = nullptr,
-                              void* cmb_out = nullptr) {
+                              bool prefetch = false, unsigned long long* itrace = nullptr) {
   FfnParams p;
   p.map_gu = c->map_gu;
   p.map_d = c->map_d;
@@ -889,11 +885,6 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   }
   p.shared_row0 = N * c->k;
   p.shared_tok0 = 0;
-  p.cmb_out = (cmb_out && !ep_local) ? cmb_out : nullptr;  // a10 in the phase-2 epilogue
-  p.cmb_cnt = c->cmb_cnt;
-  p.cmb_topk = c->topk;
-  p.cmb_slot = c->pair_slot;
-  p.cmb_gates = c->gates;
   if (ep_local) {  // local experts over all ranks' rows; shared expert on this rank's tokens
     p.map_x = c->map_x_all;
     p.off_out = c->off_l;
@@ -963,7 +954,7 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   BookParams b;
   b.cnt = cnt;
   b.par = par;
-  b.pf_list = (c->pf_target && !E_override) ? c->pf_list : nullptr;
+  b.pf_list = c->pf_target ? c->pf_list : nullptr;  // EP: local expert indices
   b.pf_n = c->pf_n;
   b.pf_by_hits = c->knob_pf_by_hits ? 1 : 0;
   b.mask = c->mask;
@@ -1020,8 +1011,6 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.g_cnt = c->g_cnt;
   rp.zero_i = c->ffn_ctrl;
   rp.n_zero = 2 + c->max_entries;
-  rp.zero_c = c->cmb_cnt;
-  rp.n_zero_c = c->ep ? 0 : N * ((H + kTileM - 1) / kTileM);
   rp.trace = (dbg && dbg->route_trace) ? reinterpret_cast<unsigned long long*>(dbg->route_trace)
                                        : nullptr;
   rp.ep_P = 0;
@@ -1395,14 +1384,12 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     CU_TRY(cudaEventRecord(rec.ev[3], st));
   }
   // ---------------- a7/a9 FFN over the hit experts already in HBM (+ shared expert)
-  const bool fused_combine = !pool_mode && c->knob_fused_combine;
   if (N > 0) {
     s = launch_ffn(c, c->cnt, pool_mode ? c->slot_of_dev : nullptr, nullptr, nullptr, c->ffn_ctrl,
                    c->ffn_ctrl + 1, N, st, false,
                    dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) : nullptr, c->cnt_par,
                    !pool_mode,
-                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_item_trace) : nullptr,
-                   fused_combine ? out : nullptr);
+                   dbg ? reinterpret_cast<unsigned long long*>(dbg->ffn_item_trace) : nullptr);
     if (s != TIDE_OK) return s;
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
@@ -1423,18 +1410,18 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
 
-  // ---------------- a10 combine (separate kernel when it is not fused into the FFN)
-  if (N > 0 && !fused_combine) {
+  // ---------------- a10 combine
+  if (N > 0) {
     const dim3 grid(N, (H + 511) / 512);
     unsigned long long* ctr =  // debug: [6] latest start, [7] latest end in CTA 0's FFN record
         (dbg && dbg->ffn_trace) ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) + 6 : nullptr;
     if (c->bf16)
-      CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), 0, st,
+      CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), sizeof(int) * E, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
                         static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr));
     else
-      CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), 0, st,
+      CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), sizeof(int) * E, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
                         static_cast<float*>(out), N, k, H, shared ? 1 : 0, ctr));
@@ -1554,7 +1541,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   CU_TRY(cudaEventRecord(c->ev_book, c->side));
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[3], st));
   // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
-  s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true);
+  s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true,
+                 nullptr, nullptr, /*prefetch: the next layer's local experts into L2*/ true);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
   // a10: per-source partial sums, exchange, rank-order sum

@@ -301,27 +301,3 @@ def test_placement_over_capacity_device_all_leaves_placement_unchanged():
     assert pout.cpu().numpy().tolist() == [1] * 12
     ref = oracle.moe_step(layer.oracle_layer(), x_np, SMALL.top_k, np.zeros(12, np.uint8), 0, 1, 12)
     assert (hits.cpu().numpy() == ref.hits).all()
-
-
-@pytest.mark.parametrize("shape_name", ["mini", "sweep"])
-def test_fused_combine_bitwise_equals_combine_kernel(shape_name):
-    """a10 fused into the FFN's phase-2 epilogue (last contributor of each (token, H-tile)
-    slice) uses the combine kernel's arithmetic element for element, so the two paths give
-    bitwise identical outputs (the fused path via TIDE_FUSED_COMBINE, read at context creation)."""
-    import os
-    from paper_2605_20179_b200 import tide
-    shape = g.SHAPES[shape_name]
-    layer = DeviceLayer(shape, 37)
-    xs = g.block_hidden_np(shape, 37, steps=3)
-    sep = tide.Context(desc_for(shape), shape.num_experts)
-    os.environ["TIDE_FUSED_COMBINE"] = "1"
-    try:
-        fused = tide.Context(desc_for(shape), shape.num_experts)
-    finally:
-        del os.environ["TIDE_FUSED_COMBINE"]
-    E = shape.num_experts
-    for t in range(3):
-        x = g.np_to_torch(xs[t], "cuda")
-        a = _out_bytes(fused, layer, x, np.zeros(E, np.uint8), t, 1, E)
-        b = _out_bytes(sep, layer, x, np.zeros(E, np.uint8), t, 1, E)
-        assert (a == b).all(), t
