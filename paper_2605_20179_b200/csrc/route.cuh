@@ -101,6 +101,9 @@ struct RouteParams {
   int n_zero_j;
   // peer-memory EP: the grid's last CTA builds the local experts' lists (route_ep_lists)
   int ep_lists, ep_e0, ep_El, ep_rows;  // rows = P * maxN
+  int ep_shared_dev;           // a peer rank runs on this GPU (one-process emulation or two
+                               // processes on one device): the FFN may launch only after the
+                               // lists exist (R-22); otherwise it launches early, as without EP
   int* ep_cnt_l;               // [El] counts over every rank's rows (zeroed via zero_j)
   int* ep_list_l;              // [El][rows] x_all row of each list slot
   int* ep_pslot;               // [rows * k] slot of each pair (-1: not a local expert)
@@ -284,6 +287,7 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
 // parity's dispatch / combine counters for the next step (their last readers are done).
 // A wait that gives up after 20 s records the failure in the error word and returns.
 __device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, int& s_last) {
+  __shared__ int s_ok;  // the wait's outcome (not s_last: other threads may still be reading it)
   __syncthreads();  // s_last was set by thread 0
   if (!s_last) return;
   char* sym = p.ep_base[p.ep_rank];
@@ -309,10 +313,10 @@ __device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, in
       ctr[par] = 0u;
       ctr[2 + par] = 0u;
     }
-    s_last = ok;
+    s_ok = ok;
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_ok) return;
   const int k = p.k, maxN = p.maxN, e0 = p.ep_e0, El = p.ep_El;
   const int* topk_all = reinterpret_cast<const int*>(sym + p.ep_off_topk);
   const int* ntok = reinterpret_cast<const int*>(sym + p.ep_off_ntok);
@@ -330,7 +334,7 @@ __device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, in
       p.ep_pslot[q] = -1;
     }
   }
-  pdl_trigger();  // the grid's other CTAs have exited: the FFN may launch now
+  if (p.ep_shared_dev) pdl_trigger();  // the grid's other CTAs have exited: the FFN may launch now
 }
 
 // Shared tail of both route kernels: arrive on the token group's counter; the group's last
@@ -459,9 +463,9 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   const int E = p.E, N = p.N, H = p.H;
   const int n0 = blockIdx.y * p.tpc, n1 = min(N, n0 + p.tpc);
   pdl_wait();     // X may be written by the previous kernel in the stream
-  // let the FFN grid start its prologue; peer-memory EP: only once the local lists exist
-  // (route_ep_lists), so a resident FFN never holds SMs a waited-on peer still needs
-  if (!p.ep_lists) pdl_trigger();
+  // let the FFN grid start its prologue; peer-memory EP with a peer on this GPU: only once the
+  // local lists exist (route_ep_lists), so a resident FFN never holds SMs that peer still needs
+  if (!p.ep_lists || !p.ep_shared_dev) pdl_trigger();
   unsigned long long* tr =
       p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   const int S = p.ksplit, ks = blockIdx.x % S;  // this CTA's slice of H (S slices per tile)
   const int n0 = blockIdx.y * 8, n1 = min(N, n0 + 8), e0 = (blockIdx.x / S) * 16;
   pdl_wait();
-  if (!p.ep_lists) pdl_trigger();  // see tide_route_kernel
+  if (!p.ep_lists || !p.ep_shared_dev) pdl_trigger();  // see tide_route_kernel
   unsigned long long* tr =
       p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && tid == 0) { tr[0] = globaltimer_ns(); tr[1] = tr[2] = tr[3] = tr[4] = tr[5] = tr[6] = 0; }

@@ -211,6 +211,7 @@ struct tide_ctx {
   CUtensorMap map_x_all;
   // peer-memory EP (tide_ctx_create_ep_p2p): x_all/topk_all/gates_all/recv live in `sym`
   bool p2p = false, connected = false;
+  bool peer_same_device = false;  // a peer's symmetric region lives on this GPU (R-22)
   char* sym = nullptr;
   EpSymLayout lay{};
   EpPeers peers{};
@@ -638,6 +639,16 @@ tide_status tide_ctx_ep_export(tide_ctx* c, void* handle, void** base) {
   return TIDE_OK;
 }
 
+// Whether device memory at ptr is allocated on `device` (a peer sharing this GPU).
+static bool on_device(const void* ptr, int device) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;  // unknown: take the safe (deferred-trigger) protocol
+  }
+  return a.device == device;
+}
+
 tide_status tide_ctx_ep_connect(tide_ctx* c, const void* handles, const void* const* bases) {
   if (!c || !c->p2p) return fail(TIDE_EINVAL, "not a peer-memory EP context");
   if (c->connected && c->world > 1) return fail(TIDE_EINVAL, "context already connected");
@@ -647,6 +658,7 @@ tide_status tide_ctx_ep_connect(tide_ctx* c, const void* handles, const void* co
     if (p == c->rank) continue;
     if (bases && bases[p]) {
       c->peers.base[p] = static_cast<char*>(const_cast<void*>(bases[p]));
+      c->peer_same_device = c->peer_same_device || on_device(bases[p], c->device);
       continue;
     }
     if (!handles) return fail(TIDE_EINVAL, "no handle or base for rank %d", p);
@@ -656,6 +668,7 @@ tide_status tide_ctx_ep_connect(tide_ctx* c, const void* handles, const void* co
     CU_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
     c->ipc_opened.push_back(ptr);
     c->peers.base[p] = static_cast<char*>(ptr);
+    c->peer_same_device = c->peer_same_device || on_device(ptr, c->device);
   }
   c->connected = true;
   return TIDE_OK;
@@ -1018,6 +1031,7 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
   rp.zero_j = nullptr;
   rp.n_zero_j = 0;
   rp.ep_lists = 0;
+  rp.ep_shared_dev = 0;
   if (c->p2p) {  // peer-memory EP: the router dispatches (route.cuh)
     rp.ep_P = c->world;
     rp.ep_rank = c->rank;
@@ -1030,6 +1044,7 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
     rp.zero_j = c->cnt_l;
     rp.n_zero_j = c->El;
     rp.ep_lists = 1;  // the local experts' lists are built by the route grid's last CTA
+    rp.ep_shared_dev = c->peer_same_device ? 1 : 0;
     rp.ep_e0 = c->e0;
     rp.ep_El = c->El;
     rp.ep_rows = c->rows_all;

@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 tr = r.debug["route_trace"].cpu().numpy().reshape(-1, 8).astype(np.int64)
 tpc = 4 if N <= 64 else 8
 ny = max(1, (N + tpc - 1) // tpc)
-tr = tr[: ((E + 7) // 8) * ny]
+tr = tr[tr[:, 0] > 0]  # the CTAs the launched grid had (CUDA-core or tensor-core router)
 t0 = tr[:, 0].min()
 print(f"{shape.name}: {len(tr)} CTAs")
 print(f"  start spread       {(tr[:, 0].max() - t0) / 1e3:7.2f} us")
@@ -37,3 +37,7 @@ print(f"  phase2 CTAs        {len(last)}")
 print(f"  phase2 start (min/max) {(last[:, 2].min() - t0) / 1e3:7.2f} / {(last[:, 2].max() - t0) / 1e3:7.2f} us")
 print(f"  phase2 end   (max)     {(last[:, 3].max() - t0) / 1e3:7.2f} us")
 print(f"  phase2 duration median {np.median(last[:, 3] - last[:, 2]) / 1e3:7.2f} us")
+for i, name in ((4, "logits in"), (5, "selection done"), (6, "histogram done")):
+    v = last[last[:, i] > 0]
+    if len(v):
+        print(f"  phase2 {name:15s} median {np.median(v[:, i] - v[:, 2]) / 1e3:7.2f} us after its start")

@@ -33,6 +33,7 @@ ap.add_argument("--layers", type=int, default=2)
 ap.add_argument("--caps", default="64,128,192,256")
 ap.add_argument("--taus", default="1,2,3,4,6,8,12,16")
 ap.add_argument("--out", default="profiles/r02/sweep_interval.json")
+ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 s = g.SWEEP
 E, k, H, F, N, T = s.num_experts, s.top_k, s.hidden, s.ffn, s.tokens, s.steps
@@ -82,26 +83,41 @@ res = {"workload": "BJ.configs[4]: mini shape, 8 blocks (256 tokens) per layer-s
                    f"{a.layers} layers, T={T}, pinned-host serving (host_master), calibrated routing",
        "h2d_us_per_expert": c_io * 1e6, "runs": [], "model": []}
 taus = [int(v) for v in a.taus.split(",")]
-for C in [int(v) for v in a.caps.split(",")]:
-    for tau in taus:
-        ctxs = [tide.Context(desc, C, 16) for _ in layers]
-        pls = [torch.zeros(E, dtype=torch.uint8, device=dev) for _ in layers]
-        st = dict(copies=0, h2d=0, resident_pairs=0, pairs=0)
-        torch.cuda.synchronize()
-        e0.record()
-        for t in range(T):
-            for L, c, p in zip(layers, ctxs, pls):
-                r = c.moe_step(L["x"][t], L["wr"], host_master=L["host"], shared_w=L["shared"],
-                               placement=p, step=t, interval=tau, placement_out=p, stats=True)
+def run_block(ctxs, pls, tau, st=None):
+    for t in range(T):
+        for L, c, p in zip(layers, ctxs, pls):
+            r = c.moe_step(L["x"][t], L["wr"], host_master=L["host"], shared_w=L["shared"],
+                           placement=p, step=t, interval=tau, placement_out=p, stats=st is not None)
+            if st is not None:
                 st["copies"] += r.stats["copies"]
                 st["h2d"] += r.stats["h2d_bytes"]
                 st["resident_pairs"] += r.stats["resident_pairs"]
                 st["pairs"] += N * k
-        e1.record()
+
+
+# every cell: one untimed warm-up block (slot pool and staging ring allocated, placement at its
+# steady state), then `--reps` timed blocks, each continuing from the previous block's
+# placement; the cell's time is the median block (host-side stalls show up as outliers)
+for C in [int(v) for v in a.caps.split(",")]:
+    for tau in taus:
+        ctxs = [tide.Context(desc, C, 16) for _ in layers]
+        pls = [torch.zeros(E, dtype=torch.uint8, device=dev) for _ in layers]
+        run_block(ctxs, pls, tau)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        times, stats = [], []
+        for _ in range(a.reps):
+            st = dict(copies=0, h2d=0, resident_pairs=0, pairs=0)
+            e0.record()
+            run_block(ctxs, pls, tau, st)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            stats.append(st)
+        i_med = int(np.argsort(times)[len(times) // 2])
+        ms, st = times[i_med], stats[i_med]
         ls = T * len(layers)
         row = {"capacity": C, "interval": tau, "ms_per_layer_step": ms / ls,
+               "ms_per_layer_step_blocks": [round(v / ls, 4) for v in times],
                "block_tokens_per_s": N * ls / (ms / 1e3),
                "h2d_experts_per_layer_step": st["copies"] / ls,
                "h2d_GBps": st["h2d"] / (ms / 1e3) / 1e9,
@@ -110,7 +126,7 @@ for C in [int(v) for v in a.caps.split(",")]:
         print(json.dumps(row), flush=True)
         del ctxs
 
-# the step without expert I/O: the C = E run minus its (cold-start) copies at the H2D rate
+# the step without expert I/O: the C = E run (warm: no copies) minus any copies at the H2D rate
 ref = next(r for r in res["runs"] if r["capacity"] == E and r["interval"] == 1)
 c_step = max(0.0, ref["ms_per_layer_step"] / 1e3 - c_io * ref["h2d_experts_per_layer_step"])
 for C in [int(v) for v in a.caps.split(",")]:
