@@ -386,6 +386,33 @@ TIDE_API tide_status tide_interval_cost_trace(const tide_interval_trace_model* m
 TIDE_API tide_status tide_optimize_interval_trace(const tide_interval_trace_model* m,
                                                   int32_t* tau_out, double* curve);
 
+/* NEXT-2 replay (DESIGN R-24): the exact expert copies of a refresh interval on a recorded
+ * routing trace, instead of the stationary lag averages above.  Alg. 1 lines 3-4
+ * are replayed step by step with the rules the library's own host_master step applies:
+ * refresh iff t % tau == 0 within the block (a4), placement = top-B by (hits desc, id asc)
+ * (R-5, R-8), copies: a hit expert not in HBM at the step's start is copied once (into its
+ * slot if it is placed, else through staging: R-13), a placed expert with no hits is copied
+ * at the refresh unless lazy (R-9), an evicted expert stays servable until the step ends
+ * (R-12).  `passes` blocks of the same trace run back to back with the placement carried
+ * across blocks (nothing in HBM before the first block); *copies is the total of the last
+ * pass (passes >= 2: steady state), copies_per_step (host [T] or NULL) its per-step split.
+ *  counts : host [T][E] int32 hit counts of one block (e.g. hit_counts of T steps)
+ * Constraints: T >= 1, 1 <= B <= E, tau >= 1, passes >= 1; else TIDE_EINVAL.
+ * NEXT-1 counter modes / incumbent ties are not replayed (mode 0 only).               */
+TIDE_API tide_status tide_interval_replay(const int32_t* counts, int32_t T, int32_t E, int32_t B,
+                                          int32_t tau, int32_t lazy, int32_t passes,
+                                          int64_t* copies, int32_t* copies_per_step);
+/* Eq. 7 over the replay: cost(tau) = c_io * copies(tau) + T * c_step for tau = 1..tau_max
+ * (exhaustive, ties -> smallest tau); curve: host [tau_max] costs or NULL.             */
+typedef struct {
+  const int32_t* counts;  /* host [T][E] */
+  int32_t T, E, B, lazy, passes;
+  double c_io, c_step;
+} tide_interval_replay_model;
+TIDE_API tide_status tide_optimize_interval_replay(const tide_interval_replay_model* m,
+                                                   int32_t tau_max, int32_t* tau_out,
+                                                   double* curve);
+
 /* NEXT-4: routing-trace analytics on the device.
  *  counts : device [T][E] int32 per-step hit counts (e.g. hit_counts of T steps)
  *  sim    : device [T][T] fp64 cosine similarity of the count vectors (0 if a vector is 0)

@@ -373,6 +373,19 @@ def interval_profile(counts, B):
     return miss, mig
 
 
+def interval_replay(counts, B, tau, lazy=False, passes=2):
+    """NEXT-2 replay (R-24): (copies of the last pass, copies per step [T]) of a [T, E] trace."""
+    c = np.ascontiguousarray(counts, np.int32)
+    T, E = c.shape
+    per = np.zeros(T, np.int32)
+    f = _d("orc_interval_replay")
+    f.restype = ctypes.c_long
+    f.argtypes = [ctypes.c_int] * 6 + [ctypes.c_void_p, ctypes.c_void_p]
+    tot = f(T, E, B, tau, int(lazy), passes, _p(c), _p(per))
+    assert tot >= 0
+    return int(tot), per
+
+
 def interval_copies_trace(T, tau, miss_lag, mig_lag):
     f = _d("orc_interval_copies_trace")
     f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]

@@ -516,3 +516,35 @@ double orc_interval_copies_trace(int T, int tau, const double* miss_lag, const d
   for (int j = 0; j < tau; ++j) per += miss_lag[j];
   return (double)T / (double)tau * per;
 }
+
+/* ---------------- NEXT-2 replay (DESIGN R-24): the copies an interval causes on a trace ----
+ * Alg. 1 lines 3-4 run step by step over a recorded routing trace: at every
+ * step t of a block, refresh iff t % tau == 0 (O3), placement by O6 (R-5 current-step
+ * counts, R-8 ties), expert copies by O10 (R-9 eager/lazy, R-12 eviction after the step,
+ * R-13 streaming).  `passes` blocks of the same trace run back to back, the placement and
+ * the loaded set carried from block to block, nothing loaded before the first block;
+ * the copies of the LAST pass are returned (per step in copies_per_step, may be NULL).   */
+long orc_interval_replay(int T, int E, int B, int tau, int lazy, int passes,
+                         const int32_t* counts, int32_t* copies_per_step) {
+  if (T < 1 || E < 1 || B < 1 || B > E || tau < 1 || passes < 1) return -1;
+  uint8_t* pl = (uint8_t*)calloc((size_t)E, 1);
+  uint8_t* npl = (uint8_t*)calloc((size_t)E, 1);
+  uint8_t* loaded = (uint8_t*)calloc((size_t)E, 1);
+  long total = 0;
+  for (int pass = 0; pass < passes; ++pass)
+    for (int t = 0; t < T; ++t) {
+      const int32_t* hits = counts + (size_t)t * E;
+      orc_placement(E, B, hits, orc_is_refresh(t, tau), pl, npl);
+      orc_io io;
+      orc_io_step(E, lazy, hits, pl, npl, loaded, &io);
+      memcpy(pl, npl, (size_t)E);
+      if (pass == passes - 1) {
+        total += io.copies;
+        if (copies_per_step) copies_per_step[t] = io.copies;
+      }
+    }
+  free(pl);
+  free(npl);
+  free(loaded);
+  return total;
+}

@@ -152,6 +152,9 @@ double orc_drift(int E, int B, const int32_t* prev, const int32_t* cur);
 int orc_interval_profile(int T, int E, int B, const int32_t* counts, double* miss_lag,
                          double* mig_lag);
 double orc_interval_copies_trace(int T, int tau, const double* miss_lag, const double* mig_lag);
+/* NEXT-2 replay (R-24): copies of the last of `passes` back-to-back blocks of the trace. */
+long orc_interval_replay(int T, int E, int B, int tau, int lazy, int passes,
+                         const int32_t* counts, int32_t* copies_per_step);
 
 #ifdef __cplusplus
 }

@@ -1730,6 +1730,67 @@ tide_status tide_optimize_interval_trace(const tide_interval_trace_model* m, int
   return TIDE_OK;
 }
 
+// NEXT-2 replay (R-24): the host_master step's placement and copy rules over a trace.
+tide_status tide_interval_replay(const int32_t* counts, int32_t T, int32_t E, int32_t B,
+                                 int32_t tau, int32_t lazy, int32_t passes, int64_t* copies,
+                                 int32_t* copies_per_step) {
+  if (!counts || !copies) return fail(TIDE_EINVAL, "null argument");
+  if (T < 1 || E < 1 || B < 1 || B > E || tau < 1 || passes < 1)
+    return fail(TIDE_EINVAL, "T %d / E %d / B %d / tau %d / passes %d", T, E, B, tau, passes);
+  std::vector<uint8_t> placed(E, 0), in_hbm(E, 0);
+  std::vector<int> ids(E);
+  int64_t total = 0;
+  for (int pass = 0; pass < passes; ++pass)
+    for (int t = 0; t < T; ++t) {
+      const int32_t* c = counts + (size_t)t * E;
+      if (t % tau == 0) {  // refresh: top-B by (hits desc, id asc)
+        for (int e = 0; e < E; ++e) ids[e] = e;
+        std::stable_sort(ids.begin(), ids.end(), [c](int a, int b) { return c[a] > c[b]; });
+        std::fill(placed.begin(), placed.end(), 0);
+        for (int i = 0; i < B; ++i) placed[ids[i]] = 1;
+      }
+      int n = 0;
+      for (int e = 0; e < E; ++e) {
+        if (in_hbm[e]) {  // served from its slot; an evicted slot is freed after the step
+          in_hbm[e] = placed[e];
+        } else if (placed[e] && (c[e] > 0 || !lazy)) {  // promoted: copied into its slot
+          ++n;
+          in_hbm[e] = 1;
+        } else if (c[e] > 0) {  // streamed through staging for this step only
+          ++n;
+        }
+      }
+      if (pass == passes - 1) {
+        total += n;
+        if (copies_per_step) copies_per_step[t] = n;
+      }
+    }
+  *copies = total;
+  return TIDE_OK;
+}
+
+tide_status tide_optimize_interval_replay(const tide_interval_replay_model* m, int32_t tau_max,
+                                          int32_t* tau_out, double* curve) {
+  if (!m || !tau_out) return fail(TIDE_EINVAL, "null argument");
+  if (tau_max < 1) return fail(TIDE_EINVAL, "tau_max %d < 1", tau_max);
+  int best = 1;
+  double best_c = 0.0;
+  for (int tau = 1; tau <= tau_max; ++tau) {  // Eq. 7, exhaustive
+    int64_t cp = 0;
+    tide_status s = tide_interval_replay(m->counts, m->T, m->E, m->B, tau, m->lazy, m->passes,
+                                         &cp, nullptr);
+    if (s != TIDE_OK) return s;
+    const double c = m->c_io * (double)cp + (double)m->T * m->c_step;
+    if (curve) curve[tau - 1] = c;
+    if (tau == 1 || c < best_c) {
+      best = tau;
+      best_c = c;
+    }
+  }
+  *tau_out = best;
+  return TIDE_OK;
+}
+
 // ---------------------------------------------------------------- NEXT-4 (device)
 tide_status tide_trace_stats(const int32_t* counts, int32_t T, int32_t E, int32_t B, double* sim,
                              int32_t* unique, double* drift, void* stream) {

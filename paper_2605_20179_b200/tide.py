@@ -33,7 +33,8 @@ EXPORTED = ("tide_abi_version", "tide_build_sm", "tide_last_error", "tide_expert
             "tide_interval_cost", "tide_optimize_interval", "tide_trace_stats",
             "tide_ctx_create_ep_p2p", "tide_ep_handle_bytes", "tide_ctx_ep_export",
             "tide_ctx_ep_connect", "tide_ctx_ep_error", "tide_ctx_ep_wait", "tide_interval_profile",
-            "tide_interval_cost_trace", "tide_optimize_interval_trace")
+            "tide_interval_cost_trace", "tide_optimize_interval_trace", "tide_interval_replay",
+            "tide_optimize_interval_replay")
 
 
 class TideError(RuntimeError):
@@ -89,6 +90,12 @@ class IntervalModel(ctypes.Structure):
 class IntervalTraceModel(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int32), ("c_io", ctypes.c_double), ("c_step", ctypes.c_double),
                 ("miss_lag", ctypes.c_void_p), ("mig_lag", ctypes.c_void_p)]
+
+
+class IntervalReplayModel(ctypes.Structure):
+    _fields_ = [("counts", ctypes.c_void_p), ("T", ctypes.c_int32), ("E", ctypes.c_int32),
+                ("B", ctypes.c_int32), ("lazy", ctypes.c_int32), ("passes", ctypes.c_int32),
+                ("c_io", ctypes.c_double), ("c_step", ctypes.c_double)]
 
 
 _lib = None
@@ -157,6 +164,11 @@ def lib():
                                                ctypes.POINTER(ctypes.c_double)]
         L.tide_optimize_interval_trace.argtypes = [ctypes.POINTER(IntervalTraceModel),
                                                    ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]
+        L.tide_interval_replay.argtypes = [ctypes.c_void_p] + [ctypes.c_int32] * 6 + [
+            ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p]
+        L.tide_optimize_interval_replay.argtypes = [ctypes.POINTER(IntervalReplayModel),
+                                                    ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                                    ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -491,4 +503,30 @@ def optimize_interval_trace(T, c_io, c_step, miss_lag, mig_lag):
     curve = np.zeros(max(1, T - 1), np.float64)
     _check(lib().tide_optimize_interval_trace(ctypes.byref(m), ctypes.byref(tau),
                                               ctypes.c_void_p(curve.ctypes.data)))
+    return tau.value, curve
+
+
+def interval_replay(counts, B: int, tau: int, lazy: bool = False, passes: int = 2):
+    """tide_interval_replay on a host [T, E] int32 trace -> (copies of the last pass, [T])."""
+    import numpy as np
+    c = np.ascontiguousarray(counts, np.int32)
+    T, E = c.shape
+    per = np.zeros(T, np.int32)
+    cp = ctypes.c_int64()
+    _check(lib().tide_interval_replay(ctypes.c_void_p(c.ctypes.data), T, E, B, tau, int(lazy),
+                                      passes, ctypes.byref(cp), ctypes.c_void_p(per.ctypes.data)))
+    return cp.value, per
+
+
+def optimize_interval_replay(counts, B: int, c_io: float, c_step: float, tau_max: int,
+                             lazy: bool = False, passes: int = 2):
+    """tide_optimize_interval_replay -> (tau*, [cost for tau = 1..tau_max])."""
+    import numpy as np
+    c = np.ascontiguousarray(counts, np.int32)
+    T, E = c.shape
+    m = IntervalReplayModel(ctypes.c_void_p(c.ctypes.data), T, E, B, int(lazy), passes, c_io, c_step)
+    tau = ctypes.c_int32()
+    curve = np.zeros(tau_max, np.float64)
+    _check(lib().tide_optimize_interval_replay(ctypes.byref(m), tau_max, ctypes.byref(tau),
+                                               ctypes.c_void_p(curve.ctypes.data)))
     return tau.value, curve

@@ -119,3 +119,30 @@ def test_h2d_prefetch_is_bitwise_neutral_and_used():
     for (a, ha, pa), (b, hb, pb) in zip(base, got):
         assert (a == b).all() and (ha == hb).all() and (pa == pb).all()
     assert c1 > 0 and c0 > 0
+
+
+@pytest.mark.parametrize("tau,lazy", [(1, False), (3, False), (4, True), (8, False)])
+def test_interval_replay_predicts_measured_copies(tau, lazy):
+    """NEXT-2 replay (R-24): the expert copies the host_master step issued over a block (the
+    second of two back-to-back blocks, placement carried across) equal the replay of the
+    GPU's own captured routing exactly, per step."""
+    from paper_2605_20179_b200 import tide
+    shape = g.Shape("rp", 64, 4, 256, 128, 1, 48, steps=12, dtype="bf16", shared_expert=True)
+    E, C = shape.num_experts, 20
+    layer = DeviceLayer(shape, 71, host_master=True)
+    ctx = tide.Context(tide.make_desc(E, 4, 256, 128, 48, shared_expert=True, lazy_promote=lazy), C, 8)
+    xs = g.block_hidden_np(shape, 71)
+    pl = torch.zeros(E, dtype=torch.uint8, device="cuda")
+    counts = np.zeros((shape.steps, E), np.int32)
+    measured = np.zeros(shape.steps, np.int64)
+    for blk in range(2):
+        for t in range(shape.steps):
+            r = ctx.moe_step(g.np_to_torch(xs[t], "cuda"), layer.router, **layer.weights("host_master"),
+                             placement=pl, step=t, interval=tau, placement_out=pl, stats=True)
+            torch.cuda.synchronize()
+            if blk == 1:
+                counts[t] = r.hit_counts.cpu().numpy()
+                measured[t] = r.stats["copies"]
+    tot, per = tide.interval_replay(counts, C, tau, lazy, 2)
+    assert per.tolist() == measured.tolist() and tot == measured.sum()
+    assert oracle.interval_replay(counts, C, tau, lazy, 2)[1].tolist() == measured.tolist()

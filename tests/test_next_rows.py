@@ -212,3 +212,90 @@ def test_library_interval_trace_matches_oracle(seed):
     ref = [1e-4 * oracle.interval_copies_trace(T, t, m1, g1) + T * 1e-5 for t in range(1, T)]
     assert np.allclose(curve, ref, rtol=1e-12)
     assert tau == 1 + int(np.argmin(ref))
+
+
+# ------------------------------------------------------------------ NEXT-2 replay (R-24)
+def _replay_golden():
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "interval_replay_example.json")))
+
+
+@pytest.mark.parametrize("ex", _replay_golden()["examples"], ids=lambda e: e["name"])
+def test_interval_replay_hand_worked(ex):
+    """Oracle and library vs hand-worked replays (tests/golden/interval_replay_example.json):
+    eviction timing (R-12), id ties (R-8), eager vs lazy promotion (R-9), cross-block state."""
+    from paper_2605_20179_b200 import _build
+    _build.build()
+    from paper_2605_20179_b200 import tide
+    c = np.array(ex["counts"], np.int32)
+    for cs in ex["cases"]:
+        for fn in (oracle.interval_replay, tide.interval_replay):
+            tot, per = fn(c, ex["B"], cs["tau"], bool(cs["lazy"]), cs["passes"])
+            assert per.tolist() == cs["per_step"], (fn, cs)
+            assert tot == sum(cs["per_step"])
+
+
+def _top_b(row, B):
+    order = np.lexsort((np.arange(row.size), -row.astype(np.int64)))  # hits desc, id asc
+    s = np.zeros(row.size, bool)
+    s[order[:B]] = True
+    return s
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_interval_replay_tau1_closed_form(seed):
+    """tau = 1, eager: the HBM set at a step's start is the previous step's placement, so
+    copies(t) = |P_t minus P_{t-1}| + |hit_t minus (P_t union P_{t-1})| (promotions, then the
+    streamed experts; R-12 serves a just-evicted expert), P_{-1} = the block's last step in
+    the second pass.  Set algebra on numpy lexsort top-B, independent of the step loop."""
+    rng = np.random.default_rng(300 + seed)
+    T, E = int(rng.integers(2, 20)), int(rng.integers(2, 64))
+    B = int(rng.integers(1, E + 1))
+    c = rng.poisson(rng.uniform(0.2, 2), (T, E)).astype(np.int32)
+    P = [_top_b(c[t], B) for t in range(T)]
+    want = []
+    for t in range(T):
+        prev = P[t - 1]  # t = 0: the previous block's last placement (pass 2)
+        want.append(int((P[t] & ~prev).sum() + ((c[t] > 0) & ~(P[t] | prev)).sum()))
+    tot, per = oracle.interval_replay(c, B, 1, False, 2)
+    assert per.tolist() == want and tot == sum(want)
+
+
+def test_interval_replay_invariants():
+    """B = E: nothing is copied once every expert is in HBM (pass 2 = 0); the cold block
+    copies all E experts at step 0 when eager, and each hit expert exactly once (its first
+    hit) when lazy.  A constant trace copies only its streamed experts in steady state."""
+    rng = np.random.default_rng(11)
+    T, E = 9, 40
+    c = rng.poisson(0.6, (T, E)).astype(np.int32)
+    for tau in (1, 2, 5, 9):
+        for lazy in (False, True):
+            assert oracle.interval_replay(c, E, tau, lazy, 2)[0] == 0
+        tot, per = oracle.interval_replay(c, E, tau, False, 1)
+        assert per[0] == E and tot == E
+        tot, per = oracle.interval_replay(c, E, tau, True, 1)
+        assert tot == int((c > 0).any(axis=0).sum())
+    row = rng.integers(0, 4, E).astype(np.int32)
+    const = np.tile(row, (T, 1))
+    for tau in (1, 3, 9):
+        tot, per = oracle.interval_replay(const, 7, tau, False, 2)
+        assert (per == (row > 0).sum() - ((row > 0) & _top_b(row, 7)).sum()).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_library_interval_replay_matches_oracle(seed):
+    from paper_2605_20179_b200 import tide
+    rng = np.random.default_rng(400 + seed)
+    T, E = int(rng.integers(2, 40)), int(rng.integers(2, 300))
+    B = int(rng.integers(1, E + 1))
+    c = rng.poisson(rng.uniform(0.1, 3), (T, E)).astype(np.int32)
+    for tau in sorted({1, 2, int(rng.integers(1, T + 1)), T}):
+        for lazy in (False, True):
+            for passes in (1, 2, 3):
+                a = oracle.interval_replay(c, B, tau, lazy, passes)
+                b = tide.interval_replay(c, B, tau, lazy, passes)
+                assert a[0] == b[0] and (a[1] == b[1]).all()
+    tau, curve = tide.optimize_interval_replay(c, B, 1e-4, 1e-5, T)
+    ref = [1e-4 * oracle.interval_replay(c, B, t)[0] + T * 1e-5 for t in range(1, T + 1)]
+    assert np.allclose(curve, ref, rtol=1e-12)
+    assert tau == 1 + int(np.argmin(ref))

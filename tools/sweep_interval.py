@@ -4,7 +4,7 @@ models against it.
 
 For every (capacity C, interval tau): one full block (T = 32 steps) of layer-steps on
 `--layers` layers, timed with CUDA events; expert H2D copies from the library's stats.
-Models (both host-side in libtide.so, both pinned against the oracle):
+Models (all host-side in libtide.so, all pinned against the oracle):
   paper  (Eq. 5-7, tide_optimize_interval): drift d measured on the GPU routing trace
          (tide_trace_stats, Eq. 4), c_io = c_miss = measured seconds per expert H2D copy
   trace  (DESIGN R-21, tide_interval_profile + tide_optimize_interval_trace): the expert
@@ -12,6 +12,9 @@ Models (both host-side in libtide.so, both pinned against the oracle):
          including the experts that stream at every step (hit but outside even a fresh
          top-C), cost = c_io * copies + T * c_step with c_step = the measured step time at
          C = E (same mode, no expert I/O after the first copies).
+  replay (DESIGN R-24, tide_interval_replay + tide_optimize_interval_replay): the exact copies
+         of each tau from the same trace, placement and copy rules replayed step by step
+         (two passes: the warm-up block, then the timed one), cost = c_io * copies + T * c_step
 The routing trace does not depend on C or tau (outputs are lossless; routing is a function
 of the inputs), so one trace per layer serves every cell.
 usage: python tools/sweep_interval.py [--layers 2] [--out profiles/r02/sweep_interval.json]
@@ -151,6 +154,22 @@ for C in [int(v) for v in a.caps.split(",")]:
                       "ms_per_step_model": round(cost / T * 1e3, 3),
                       "ms_per_step_measured": round(meas["ms_per_layer_step"], 3),
                       "cost_rel_err": round(cost / T * 1e3 / meas["ms_per_layer_step"] - 1, 4)})
+    # replay model (R-24): the exact copies of each tau on the same traces (two passes: the
+    # measurement's warm-up block, then a timed block from its placement)
+    host_tr = [tr.cpu().numpy() for tr in traces]
+    rep_cells = []
+    for tau in taus:
+        cp = sum(tide.interval_replay(tr, C, tau, False, 2)[0] for tr in host_tr) / (T * len(host_tr))
+        meas = rows[tau]
+        ms_model = (c_io * cp + c_step) * 1e3
+        rep_cells.append({"interval": tau, "copies_per_step_model": round(cp, 3),
+                          "copies_per_step_measured": round(meas["h2d_experts_per_layer_step"], 3),
+                          "ms_per_step_model": round(ms_model, 4),
+                          "ms_per_step_measured": round(meas["ms_per_layer_step"], 4),
+                          "cost_rel_err": round(ms_model / meas["ms_per_layer_step"] - 1, 4)})
+    curves = [tide.optimize_interval_replay(tr, C, c_io, c_step, max(taus))[1] for tr in host_tr]
+    curve_r = np.sum(curves, axis=0)
+    tau_r = 1 + int(np.argmin(curve_r))
     res["model"].append({
         "capacity": C, "measured_best_tau": best["interval"],
         "measured_within_1pct_of_best": near,
@@ -158,7 +177,10 @@ for C in [int(v) for v in a.caps.split(",")]:
                         "curve_ms_per_step": [round(v / T * 1e3, 3) for v in curve_p[:16]]},
         "trace_model": {"tau_star": tau_t, "c_step_ms": round(c_step * 1e3, 3),
                         "always_streamed_per_step": round(float(miss[0]), 2),
-                        "cells": cells}})
+                        "cells": cells},
+        "replay_model": {"tau_star": tau_r, "tau_star_in_measured_grid":
+                         min(taus, key=lambda t: curve_r[t - 1]),
+                         "c_step_ms": round(c_step * 1e3, 4), "cells": rep_cells}})
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"), indent=1)
 print(json.dumps(res["model"]))
