@@ -139,9 +139,11 @@ struct EpPeers {
 static_assert(kEpMaxWorld == kRouteEpMax, "route.cuh and ep.cuh disagree on the max world");
 
 struct EpSymLayout {  // byte offsets inside a rank's symmetric region
-  size_t x_all, topk_all, gates_all, ypair, hits_all, ntok, ctr, total;
+  size_t x_all, cnt_l, list_l, dst_l, ypair, hits_all, ctr, total;
+  // x_all: [P * maxN][H] token rows dispatched by every source rank (row src * maxN + n)
+  // cnt_l: [2][El] local-expert counts by step parity, appended to by every source's router
+  // list_l / dst_l: [El][P * maxN] x_all row / (source rank << 28 | pair row) of each slot
   // ypair: [maxN * k][H] fp32, y of this rank's pair (n, j) written by its expert's owner
-  // ntok: [P] tokens each source rank dispatched this step (rows >= ntok[src] are stale)
   // ctr: [0..1] dispatch arrivals by parity, [2..3] combine arrivals by parity, [4] error
 };
 

@@ -71,14 +71,14 @@ struct FfnParams {
   unsigned long long* itrace;  // debug: per CTA, 64 items x {claim, kind<<32|entry, dep met, issued}
   // Peer-memory EP (tide_ffn_kernel<T, true>): the phase-2 epilogue stores each routed pair's
   // y row straight into the owning rank's ypair[n*k + j] over peer memory -- the combine's
-  // exchange fused into the GEMM epilogue; the grid's last CTA then delivers the local
+  // exchange fused into the GEMM epilogue; every CTA then delivers a slice of the local
   // experts' counts into every rank's hits_all and arrives once on each rank's combine
-  // counter (one system-scope fence per launch).  Shared-expert rows stay local (y_out).
+  // counter after its own release.  Shared-expert rows stay local (y_out).
   int ep_P, ep_e0, ep_El;
   const unsigned* ep_dst; // [El][rows_all] per list slot: owner rank << 28 | pair row n*k + j
-  const int* ep_cnt_l;    // [El] local experts' counts (global hits of those experts)
+  const int* ep_cnt_l;    // [2][El] local experts' counts by parity (global hits of those
+                          // experts); this step's half is [par ^ 1] once the route flipped par
   const int* ep_par;      // step parity word (flipped by the route kernel)
-  int* ep_done;           // grid arrival counter (zeroed by the route kernel)
   char* ep_base[8];       // symmetric regions of every rank
   size_t ep_off_ypair, ep_off_hits, ep_off_ctr;
   int shared_row0;       // first h/y row of the shared expert's tokens (N*k single-device)
@@ -526,25 +526,27 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if constexpr (EP) {  // every CTA releases its own peer y stores at system scope as it arrives
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-      s_last = (p.ep_P > 1 ? atom_add_acq_rel_sys(p.ep_done, 1) : atom_add_acq_rel_gpu(p.ep_done, 1)) ==
-               (int)gridDim.x - 1;
+  if constexpr (EP) {
+    // every CTA (no last-CTA tail): its slice of the local experts' counts into every rank's
+    // hits_all, then one release (system scope when a peer is another GPU) covering the CTA's
+    // peer y stores (ordered before it by the barrier above) and one arrival on every rank's
+    // combine counter; the final kernel waits for the sum of the ranks' FFN grid sizes
+    const int par = __ldcg(p.ep_par);  // flipped by the route: this step's counts at [par ^ 1]
+    const int* cnt = p.ep_cnt_l + (par ^ 1) * p.ep_El;
+    const int per = (p.ep_El + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int e0 = blockIdx.x * per, e1 = min(p.ep_El, e0 + per);
+    for (int i = threadIdx.x; i < p.ep_P * (e1 - e0); i += blockDim.x) {
+      const int dst = i / (e1 - e0), e = e0 + i - dst * (e1 - e0);
+      reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_hits)[p.ep_e0 + e] = __ldcg(cnt + e);
     }
     __syncthreads();
-    if (s_last) {  // the grid's last CTA: counts to every rank, one system release, arrive
-      for (int i = threadIdx.x; i < p.ep_P * p.ep_El; i += blockDim.x) {
-        const int dst = i / p.ep_El, e = i - dst * p.ep_El;
-        reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_hits)[p.ep_e0 + e] = __ldcg(p.ep_cnt_l + e);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int par = __ldcg(p.ep_par);
+    if (threadIdx.x == 0) {
+      if (p.ep_P > 1)
         fence_release_sys();
-        for (int dst = 0; dst < p.ep_P; ++dst)
-          red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par, 1u);
-      }
+      else
+        fence_acq_rel_gpu();
+      for (int dst = 0; dst < p.ep_P; ++dst)
+        red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par, 1u);
     }
   }
 }

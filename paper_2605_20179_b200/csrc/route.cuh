@@ -94,20 +94,20 @@ struct RouteParams {
   // group's phase-2 CTA stores the group's top-k ids and gates; the grid's last CTA stores
   // this rank's token count and arrives (release, system scope) on every rank's dispatch
   // counter for the new parity.  Row of token n of this rank in x_all: ep_rank*maxN + n.
+  // Each routed pair (n, j) -> expert e is appended straight into the owning rank's token
+  // list of e (owner = e / El): a slot from an atomic on the owner's count, the token's x_all
+  // row and the pair's return address in the list -- the owners' lists are complete once
+  // every source has arrived, with no list-building pass.
   int ep_P, ep_rank;
   char* ep_base[kRouteEpMax];  // symmetric region of every rank
-  size_t ep_off_x, ep_off_topk, ep_off_gates, ep_off_ntok, ep_off_ctr;
-  int* zero_j;                 // EP: local-expert counts zeroed by CTA (0,0)
-  int n_zero_j;
-  // peer-memory EP: the grid's last CTA builds the local experts' lists (route_ep_lists)
-  int ep_lists, ep_e0, ep_El, ep_rows;  // rows = P * maxN
+  size_t ep_off_x, ep_off_ctr;
+  size_t ep_off_cnt;           // [2][El] per-parity local-expert counts (this step: [par])
+  size_t ep_off_list;          // [El][rows] x_all row of each list slot
+  size_t ep_off_dst;           // [El][rows] source rank << 28 | pair row n*k + j of each slot
+  int ep_lists, ep_El, ep_rows;  // ep_lists: the grid's last CTA waits for every source
   int ep_shared_dev;           // a peer rank runs on this GPU (one-process emulation or two
                                // processes on one device): the FFN may launch only after the
                                // lists exist (R-22); otherwise it launches early, as without EP
-  int* ep_cnt_l;               // [El] counts over every rank's rows (zeroed via zero_j)
-  int* ep_list_l;              // [El][rows] x_all row of each list slot
-  int* ep_pslot;               // [rows * k] slot of each pair (-1: not a local expert)
-  unsigned* ep_dst_l;          // [El][rows] owner rank << 28 | pair row of each list slot
 };
 
 struct BookParams {
@@ -192,7 +192,7 @@ __device__ __forceinline__ int block_scan_excl(int* a, int n, int* scratch /*33 
 // argmax over the lanes' heads (the winner pops); gates (R-2); per-expert counts, token
 // lists and bitmasks by atomics.
 template <int EPL>
-__device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int n,
+__device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int par, int n,
                                             const float (&v_in)[EPL],
                                             unsigned long long* tr = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -271,28 +271,36 @@ __device__ __forceinline__ void route_token(const RouteParams& p, int* cnt, int 
     if (lane < k) {
       p.topk_idx[(size_t)n * k + lane] = my_e;
       p.gates[(size_t)n * k + lane] = expf(my_l - m) / denom;
-      const int slot = atomicAdd(&cnt[my_e], 1);
-      p.list[(size_t)my_e * p.maxN + slot] = n;
-      p.pair_slot[(size_t)n * k + lane] = slot;
-      atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
+      if (p.ep_P) {  // append the pair to its owner's list of my_e (peer memory)
+        const int dst = my_e / p.ep_El, el = my_e - dst * p.ep_El;
+        char* b = p.ep_base[dst];
+        int* cd = reinterpret_cast<int*>(b + p.ep_off_cnt) + par * p.ep_El + el;
+        const int slot = p.ep_P > 1 ? atomicAdd_system(cd, 1) : atomicAdd(cd, 1);
+        const size_t q = (size_t)el * p.ep_rows + slot;
+        reinterpret_cast<int*>(b + p.ep_off_list)[q] = p.ep_rank * p.maxN + n;
+        reinterpret_cast<unsigned*>(b + p.ep_off_dst)[q] =
+            ((unsigned)p.ep_rank << 28) | (unsigned)(n * k + lane);
+      } else {
+        const int slot = atomicAdd(&cnt[my_e], 1);
+        p.list[(size_t)my_e * p.maxN + slot] = n;
+        p.pair_slot[(size_t)n * k + lane] = slot;
+        atomicOr(&p.mask[my_e * NW + (n >> 5)], 1u << (n & 31));
+      }
     }
     }
 }
 
-// Peer-memory EP, in the route grid's last CTA (after its dispatch arrivals): wait until all
-// P sources have dispatched this step (own included), then build the local experts' token
-// lists over every rank's rows -- counts, lists, per-pair slots and the destination of each
-// list slot's y row (owner rank << 28 | its pair row there) -- for the FFN that follows; rows
-// past a source's token count hold stale routing and are skipped.  It also frees the other
-// parity's dispatch / combine counters for the next step (their last readers are done).
-// A wait that gives up after 20 s records the failure in the error word and returns.
-__device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, int& s_last) {
+// Peer-memory EP, in the route grid's last CTA (after its own arrivals): wait until all P
+// sources have dispatched this step (own included) -- their X rows and list appends are then
+// in this rank's region -- and free the other parity's dispatch / combine counters for the
+// next step (their last readers are done).  A wait that gives up after 20 s records the
+// failure in the error word and returns.
+__device__ __forceinline__ void route_ep_wait(const RouteParams& p, int par, int& s_last) {
   __shared__ int s_ok;  // the wait's outcome (not s_last: other threads may still be reading it)
   __syncthreads();  // s_last was set by thread 0
   if (!s_last) return;
-  char* sym = p.ep_base[p.ep_rank];
-  unsigned* ctr = reinterpret_cast<unsigned*>(sym + p.ep_off_ctr);
   if (threadIdx.x == 0) {
+    unsigned* ctr = reinterpret_cast<unsigned*>(p.ep_base[p.ep_rank] + p.ep_off_ctr);
     int ok = 1;
     const unsigned* cw = ctr + (par ^ 1);
     unsigned v;
@@ -316,25 +324,7 @@ __device__ __forceinline__ void route_ep_lists(const RouteParams& p, int par, in
     s_ok = ok;
   }
   __syncthreads();
-  if (!s_ok) return;
-  const int k = p.k, maxN = p.maxN, e0 = p.ep_e0, El = p.ep_El;
-  const int* topk_all = reinterpret_cast<const int*>(sym + p.ep_off_topk);
-  const int* ntok = reinterpret_cast<const int*>(sym + p.ep_off_ntok);
-  for (int q = threadIdx.x; q < p.ep_rows * k; q += blockDim.x) {
-    const int row = q / k, src = row / maxN;
-    const bool live = row - src * maxN < __ldcg(ntok + src);
-    const int e = live ? __ldcg(topk_all + q) : -1;
-    if (e >= e0 && e < e0 + El) {
-      const int s = atomicAdd(&p.ep_cnt_l[e - e0], 1);
-      p.ep_list_l[(size_t)(e - e0) * p.ep_rows + s] = row;
-      p.ep_dst_l[(size_t)(e - e0) * p.ep_rows + s] =
-          ((unsigned)src << 28) | (unsigned)((row - src * maxN) * k + (q - row * k));
-      p.ep_pslot[q] = s;
-    } else {
-      p.ep_pslot[q] = -1;
-    }
-  }
-  if (p.ep_shared_dev) pdl_trigger();  // the grid's other CTAs have exited: the FFN may launch now
+  if (s_ok && p.ep_shared_dev) pdl_trigger();  // the grid's other CTAs have exited
 }
 
 // Shared tail of both route kernels: arrive on the token group's counter; the group's last
@@ -401,20 +391,10 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
       if (s == 1.2345e-30f) tr[7] = 1;
       if (lane == 0) tr[4] = globaltimer_ns();
     }
-    route_token<EPL>(p, cnt, n, v, (tr && n == n0) ? tr : nullptr);
+    route_token<EPL>(p, cnt, par, n, v, (tr && n == n0) ? tr : nullptr);
   }
   if (tr && tid == 0) tr[6] = globaltimer_ns();
   __syncthreads();
-  if (p.ep_P) {  // dispatch this group's routing to every rank
-    const int k = p.k, rows = n1 - n0, tot = p.ep_P * rows * k;
-    for (int i = tid; i < tot; i += blockDim.x) {
-      const int j = i % k, n = n0 + (i / k) % rows, dst = i / (k * rows);
-      const size_t q = ((size_t)p.ep_rank * p.maxN + n) * k + j;
-      reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_topk)[q] = __ldcg(p.topk_idx + (size_t)n * k + j);
-      reinterpret_cast<float*>(p.ep_base[dst] + p.ep_off_gates)[q] = __ldcg(p.gates + (size_t)n * k + j);
-    }
-    __syncthreads();
-  }
   if (tid == 0) {
     if (tr) tr[3] = globaltimer_ns();
     // every CTA has read par; EP: system-scope release of this CTA's peer top-k / gate stores
@@ -425,16 +405,18 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
       if (p.ep_P) {  // every CTA's peer stores precede this point (each CTA released them
                      // itself at world > 1; the g_cnt / g_done chains acquired them here):
-                     // one release fence at system scope, then the arrivals
-        for (int dst = 0; dst < p.ep_P; ++dst)
-          reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_ntok)[p.ep_rank] = p.N;
-        fence_release_sys();
+                     // one release fence (system scope when a peer is another GPU), then
+                     // the arrivals
+        if (p.ep_P > 1)
+          fence_release_sys();
+        else
+          fence_acq_rel_gpu();
         for (int dst = 0; dst < p.ep_P; ++dst)
           red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + (par ^ 1), 1u);
       }
     }
   }
-  if (p.ep_lists) route_ep_lists(p, par, s_flag);
+  if (p.ep_lists) route_ep_wait(p, par, s_flag);
 }
 
 // Peer-memory EP dispatch of X: CTA (bx, by) stores uint4 columns [bx*per, (bx+1)*per) of
@@ -474,7 +456,10 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
-    for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
+    if (p.ep_P) {  // the next step's half of this rank's local-expert counts (see route_token)
+      int* c2 = reinterpret_cast<int*>(p.ep_base[p.ep_rank] + p.ep_off_cnt) + (par ^ 1) * p.ep_El;
+      for (int i = tid; i < p.ep_El; i += blockDim.x) c2[i] = 0;
+    }
   }
 
   // ================= phase 1: router logits (a1)
@@ -482,7 +467,7 @@ __global__ void __launch_bounds__(kRouteThreads) tide_route_kernel(const __grid_
     constexpr int G = 8;  // 16-byte chunks in flight per lane per group
     const int e = blockIdx.x * kRouterWarps + warp;
     const int chunks = H * (int)sizeof(T) / 16;
-    const bool copy_x = blockIdx.x == 0 && warp == 0;
+    const bool copy_x = blockIdx.x == 0 && warp == 0 && !p.ep_P;  // EP: x_all (push_x)
     if (e < E) {
       const uint4* wrow = reinterpret_cast<const uint4*>(static_cast<const T*>(p.wr) + (size_t)e * H);
       for (int n = n0; n < n1; n += 2) {
@@ -562,7 +547,10 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     for (int i = tid; i < E; i += blockDim.x) p.cnt2[(par ^ 1) * E + i] = 0;
     for (int i = tid; i < p.n_zero; i += blockDim.x) p.zero_i[i] = 0;
-    for (int i = tid; i < p.n_zero_j; i += blockDim.x) p.zero_j[i] = 0;
+    if (p.ep_P) {  // the next step's half of this rank's local-expert counts (see route_token)
+      int* c2 = reinterpret_cast<int*>(p.ep_base[p.ep_rank] + p.ep_off_cnt) + (par ^ 1) * p.ep_El;
+      for (int i = tid; i < p.ep_El; i += blockDim.x) c2[i] = 0;
+    }
   }
   // ================= phase 1: router logits (a1)
   {
@@ -603,8 +591,9 @@ __global__ void __launch_bounds__(kRouteThreads, MINB) tide_route_tc_kernel(cons
 #pragma unroll
     for (int r = 0; r < 4; ++r) s_red[warp][lane][r] = acc[r];
     // x_in copy (the FFN's gather source), spread over the token group's expert tiles: CTA bx
-    // copies uint4 columns [bx*per, (bx+1)*per) of the group's rows (no straggler CTA)
-    {
+    // copies uint4 columns [bx*per, (bx+1)*per) of the group's rows (no straggler CTA); under
+    // EP the FFN gathers from x_all instead (route_ep_push_x)
+    if (!p.ep_P) {
       const int per_row = H / 8;  // uint4 per row
       const int per = (per_row + (int)gridDim.x - 1) / (int)gridDim.x;
       const int q0 = blockIdx.x * per, w = min(per_row, q0 + per) - q0;

@@ -218,6 +218,7 @@ struct tide_ctx {
   std::vector<void*> ipc_opened;  // peers' regions opened with cudaIpcOpenMemHandle
   cudaEvent_t ev_ep_done = nullptr;  // the last EP step's completion (tide_ctx_ep_wait)
   unsigned* dst_l = nullptr;      // [El, rows_all] owner rank << 28 | pair row of each list slot (p2p)
+  int ep_arrivals = 0;            // p2p: combine arrivals per step = sum of the ranks' FFN grids
 
   // per-phase timing (tide_ctx_set_timing)
   bool timing = false;
@@ -363,9 +364,9 @@ void tide_ctx_destroy(tide_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->p2p) {  // these live inside the symmetric region
     c->x_all = nullptr;
-    c->topk_all = nullptr;
-    c->gates_all = nullptr;
-    c->recv = nullptr;
+    c->cnt_l = nullptr;
+    c->list_l = nullptr;
+    c->dst_l = nullptr;
     cudaFree(c->sym);
   }
   void* dev[] = {c->logits, c->topk,     c->gates,   c->pair_slot, c->cnt,    c->list,
@@ -558,29 +559,38 @@ static tide_status ctx_create_ep_impl(const tide_layer_desc* d, int32_t device,
     auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
     EpSymLayout& L = c->lay;
     L.x_all = 0;
-    L.topk_all = up(L.x_all + c->eb * (size_t)R * c->H);
-    L.gates_all = up(L.topk_all + sizeof(int) * (size_t)R * k);
-    L.ypair = up(L.gates_all + sizeof(float) * (size_t)R * k);
+    L.cnt_l = up(L.x_all + c->eb * (size_t)R * c->H);
+    L.list_l = up(L.cnt_l + sizeof(int) * 2 * (size_t)El);
+    L.dst_l = up(L.list_l + sizeof(int) * (size_t)El * R);
+    L.ypair = up(L.dst_l + sizeof(unsigned) * (size_t)El * R);
     L.hits_all = up(L.ypair + sizeof(float) * (size_t)N * k * c->H);
-    L.ntok = up(L.hits_all + sizeof(int) * (size_t)c->E);
-    L.ctr = up(L.ntok + sizeof(int) * (size_t)kEpMaxWorld);
+    L.ctr = up(L.hits_all + sizeof(int) * (size_t)c->E);
     L.total = up(L.ctr + sizeof(unsigned) * 8);
     c->p2p = true;
     ALLOC(c->sym, L.total);
-    ALLOC(c->dst_l, sizeof(unsigned) * (size_t)El * R);
     c->x_all = c->sym + L.x_all;
-    c->topk_all = reinterpret_cast<int*>(c->sym + L.topk_all);
-    c->gates_all = reinterpret_cast<float*>(c->sym + L.gates_all);
+    c->cnt_l = reinterpret_cast<int*>(c->sym + L.cnt_l);  // [2][El], by step parity
+    c->list_l = reinterpret_cast<int*>(c->sym + L.list_l);
+    c->dst_l = reinterpret_cast<unsigned*>(c->sym + L.dst_l);
     c->peers.base[rank] = c->sym;
+    {
+      const unsigned g = (unsigned)c->num_sms;  // this rank's FFN grid (read by the peers)
+      if (cudaMemcpy(c->sym + L.ctr + 5 * sizeof(unsigned), &g, sizeof(g), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+        tide_ctx_destroy(c);
+        return fail(TIDE_ECUDA, "writing the FFN grid size into the symmetric region");
+      }
+    }
     c->connected = world == 1;
+    c->ep_arrivals = c->num_sms;  // world 1: this rank's own FFN grid
   } else {
     ALLOC(c->x_all, c->eb * (size_t)R * c->H);
     ALLOC(c->topk_all, sizeof(int) * (size_t)R * k);
     ALLOC(c->gates_all, sizeof(float) * (size_t)R * k);
+    ALLOC(c->pslot_all, sizeof(int) * (size_t)R * k);
+    ALLOC(c->cnt_l, sizeof(int) * El);
+    ALLOC(c->list_l, sizeof(int) * (size_t)El * R);
   }
-  ALLOC(c->pslot_all, sizeof(int) * (size_t)R * k);
-  ALLOC(c->cnt_l, sizeof(int) * El);
-  ALLOC(c->list_l, sizeof(int) * (size_t)El * R);
   ALLOC(c->off_l, sizeof(int) * El);
   ALLOC(c->hits_l, sizeof(int) * El);
   if (!p2p) {
@@ -670,6 +680,17 @@ tide_status tide_ctx_ep_connect(tide_ctx* c, const void* handles, const void* co
     c->peers.base[p] = static_cast<char*>(ptr);
     c->peer_same_device = c->peer_same_device || on_device(ptr, c->device);
   }
+  // every rank's FFN grid arrives once per CTA on each combine counter: the wait's target is
+  // the sum of the ranks' grid sizes (each rank wrote its own into ctr[5] at creation)
+  int total = 0;
+  for (int p = 0; p < c->world; ++p) {
+    unsigned g = 0;
+    CU_TRY(cudaMemcpy(&g, c->peers.base[p] + c->lay.ctr + 5 * sizeof(unsigned), sizeof(g),
+                      cudaMemcpyDefault));
+    if (g == 0) return fail(TIDE_EINVAL, "rank %d's symmetric region has no FFN grid size", p);
+    total += (int)g;
+  }
+  c->ep_arrivals = total;
   c->connected = true;
   return TIDE_OK;
 }
@@ -880,7 +901,6 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.ep_dst = nullptr;
   p.ep_cnt_l = nullptr;
   p.ep_par = nullptr;
-  p.ep_done = nullptr;
   p.ep_off_ypair = p.ep_off_hits = p.ep_off_ctr = 0;
   for (int i = 0; i < kEpMaxWorld; ++i) p.ep_base[i] = nullptr;
   if (ep_local && c->p2p) {  // fused owner scatter of the combine (ffn.cuh)
@@ -890,7 +910,6 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
     p.ep_dst = c->dst_l;
     p.ep_cnt_l = c->cnt_l;
     p.ep_par = c->cnt_par;
-    p.ep_done = c->ffn_ctrl + 1 + c->max_entries;
     for (int i = 0; i < kEpMaxWorld; ++i) p.ep_base[i] = c->peers.base[i];
     p.ep_off_ypair = c->lay.ypair;
     p.ep_off_hits = c->lay.hits_all;
@@ -1028,8 +1047,6 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
                                        : nullptr;
   rp.ep_P = 0;
   rp.ep_rank = 0;
-  rp.zero_j = nullptr;
-  rp.n_zero_j = 0;
   rp.ep_lists = 0;
   rp.ep_shared_dev = 0;
   if (c->p2p) {  // peer-memory EP: the router dispatches (route.cuh)
@@ -1037,21 +1054,14 @@ static tide_status launch_route(tide_ctx* c, const void* x, int N, const void* w
     rp.ep_rank = c->rank;
     for (int i = 0; i < kEpMaxWorld; ++i) rp.ep_base[i] = c->peers.base[i];
     rp.ep_off_x = c->lay.x_all;
-    rp.ep_off_topk = c->lay.topk_all;
-    rp.ep_off_gates = c->lay.gates_all;
-    rp.ep_off_ntok = c->lay.ntok;
     rp.ep_off_ctr = c->lay.ctr;
-    rp.zero_j = c->cnt_l;
-    rp.n_zero_j = c->El;
-    rp.ep_lists = 1;  // the local experts' lists are built by the route grid's last CTA
+    rp.ep_off_cnt = c->lay.cnt_l;
+    rp.ep_off_list = c->lay.list_l;
+    rp.ep_off_dst = c->lay.dst_l;
+    rp.ep_lists = 1;  // the route grid's last CTA waits until every source rank dispatched
     rp.ep_shared_dev = c->peer_same_device ? 1 : 0;
-    rp.ep_e0 = c->e0;
     rp.ep_El = c->El;
     rp.ep_rows = c->rows_all;
-    rp.ep_cnt_l = c->cnt_l;
-    rp.ep_list_l = c->list_l;
-    rp.ep_pslot = c->pslot_all;
-    rp.ep_dst_l = c->dst_l;
   }
   // bf16 routers run phase 1 on the tensor cores (16 experts x 8 tokens per CTA);
   // TIDE_ROUTER_CC=1 forces the CUDA-core kernel (A/B measurement)
@@ -1551,13 +1561,14 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   CU_TRY(cudaEventRecord(c->ev_route, st));
   CU_TRY(cudaStreamWaitEvent(c->side, c->ev_route, 0));
   s = launch_book(c, c->cnt_l, placement, 0, refresh, capacity, c->hits_l, placement_out, c->side,
-                  El, step);
+                  El, step, c->p2p ? c->cnt_par : nullptr);  // p2p: [2][El] by parity
   if (s != TIDE_OK) return s;
   CU_TRY(cudaEventRecord(c->ev_book, c->side));
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[3], st));
   // a7: grouped FFN over the local experts (+ shared expert on this rank's tokens)
   s = launch_ffn(c, c->cnt_l, nullptr, nullptr, nullptr, c->ffn_ctrl, c->ffn_ctrl + 1, N, st, true,
-                 nullptr, nullptr, /*prefetch: the next layer's local experts into L2*/ true);
+                 nullptr, c->p2p ? c->cnt_par : nullptr,
+                 /*prefetch: the next layer's local experts into L2*/ true);
   if (s != TIDE_OK) return s;
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[4], st));
   // a10: per-source partial sums, exchange, rank-order sum
@@ -1565,7 +1576,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   if (c->p2p) {  // the FFN stored every pair's y at its owner and arrived (ffn.cuh)
     if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
     const dim3 grid(std::max(N, 1), nY);
-    const unsigned tgt = (unsigned)c->world;  // one FFN arrival per rank
+    const unsigned tgt = (unsigned)c->ep_arrivals;  // one arrival per FFN CTA of every rank
     if (c->bf16)
       CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<__nv_bfloat16>, grid, dim3(128), 0, st, c->sym,
                         c->lay, (const int*)c->cnt_par, tgt, (const float*)c->gates,
@@ -1611,7 +1622,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     RouteInfo local;
     std::vector<int> hl(El);
     CU_TRY(cudaMemcpyAsync(&local, c->info, sizeof(RouteInfo), cudaMemcpyDeviceToHost, st));
-    CU_TRY(cudaMemcpyAsync(hl.data(), c->cnt_l, sizeof(int) * El, cudaMemcpyDeviceToHost, st));
+    CU_TRY(cudaMemcpyAsync(hl.data(), c->hits_l, sizeof(int) * El, cudaMemcpyDeviceToHost, st));
     CU_TRY(cudaStreamSynchronize(st));
     if (local.status != 0)
       return fail(TIDE_EPLACEMENT, "step %d is not a refresh and placement holds more than %d experts",
