@@ -632,8 +632,9 @@ def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=Non
                 "unique_experts_per_layer_step": round(acc["uniq"] / layer_steps, 2),
                 "traffic_key": tkey, "traffic_detail": tdet,
                 "l2_prefetch": (f"{pf_mb:g} MB of this layer's likely experts were prefetched "
-                                "into L2 by the previous layer's FFN tail (see "
-                                "frac_prefetch_off)" if pf_mb > 0 else "off")}
+                                "into L2 by the previous layer's FFN tail and the next "
+                                f"{pf_mb / 2:g} MB by this FFN's CTAs before their wait on the "
+                                "routing (see frac_prefetch_off)" if pf_mb > 0 else "off")}
         if full and pf_mb > 0:  # control: the same launches with the cross-layer prefetch off
             st.set_prefetch(0)
             _, ph0 = st.timed(steps, warmup, phase_timing=True)

@@ -317,7 +317,9 @@ TIDE_API tide_status tide_ctx_get_timing(tide_ctx* ctx, tide_phase_times* out);
  * by hits instead), their gate/up rows (what the FFN's first items read) up to
  * budget_bytes. Each CTA of the persistent FFN issues its share once it has no more
  * work, so the prefetch fills the FFN tail, the combine and next's routing, when HBM
- * would otherwise be idle.
+ * would otherwise be idle.  `next`'s own FFN then continues the same ranked list for
+ * another budget_bytes / 2 (its persistent CTAs, resident while its routing is still being
+ * computed, issue that share before they wait on the routing).
  *   next:            the context of the layer called after `ctx` (same device); NULL or
  *                    budget_bytes == 0 disables. `next` must outlive `ctx` or be unset.
  *   next_device_all: the packed experts `next` is called with ([E, 3HF], device), or

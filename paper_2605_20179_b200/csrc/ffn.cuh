@@ -31,7 +31,6 @@ constexpr int kTileM = 128;
 constexpr int kATile = kTileM * 128;           // 16 KB: 128 rows x 128 B (one K block)
 constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 128 B
 constexpr int kStageBytes = 2 * kATile + kBTile;
-constexpr int kPfPiece = 64 * 1024;  // bytes per L2 bulk prefetch
 constexpr int kMaxEntriesSmem = 1280;          // work entries built per CTA (E + N*k/128 + ...)
 constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem;
 
@@ -49,14 +48,9 @@ struct FfnParams {
   // off[e] = prefix of counts in id order, then the shared expert (rows N*k + n).
   const int* cnt;        // [E] per-expert token counts (build mode), or [2][E] with par
   const int* par;        // nullable: route's parity word, this step's counts = cnt[par^1]
-  // NEXT-3 prefetch of the next layer (pf_base == nullptr: off)
-  const uint8_t* pf_base;  // next layer's packed experts (device_all)
-  const int* pf_list;      // next layer's experts ranked by hits at its previous step
-  const int* pf_n;         // number of ranked (hit) experts
-  int pf_max;              // budget in experts
-  long long pf_xb;         // bytes per packed expert
-  long long pf_span;       // bytes prefetched per expert, from its start (<= pf_xb)
-  const uint8_t* pf_shared;  // nullable: next layer's shared expert (prefetched first)
+  L2Prefetch pf;         // NEXT-3: issued by each CTA once it has no more work (route.cuh)
+  L2Prefetch pf_self;    // NEXT-3: this layer's likely experts past the previous layer's range,
+                         // issued before the wait on the routing (HBM is idle until then)
   const int* slot_of;    // [E] pool slot (nullptr: slot = e)
   int* off_out;          // [E] row offsets written by CTA 0 (build mode; read by combine)
   const int4* entries;   // global mode: host-built list
@@ -144,6 +138,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
   // routing (counts, token lists, x_in) comes from the preceding grid; the dependent grid
   // (combine) may launch once every CTA is past that wait, so it can read the routing it
   // needs (top-k, slots, gates) before its own wait on this grid
+  // the MMA warp is idle until the first item: while the routing is still being computed it
+  // pulls this CTA's share of this layer's likely experts (beyond what the previous layer's
+  // FFN tail prefetched) into L2
+  if (warp == 1) issue_l2_prefetch(p.pf_self, blockIdx.x + (long long)gridDim.x * lane, (long long)gridDim.x * 32);
   if (warp == 0) pdl_wait();
   __syncthreads();
   pdl_trigger();
@@ -371,21 +369,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
     // drains and the combine / next routing leave HBM idle.  Piece i of the byte range goes
     // to CTA i % grid, so the first CTAs to finish cover the first-claimed experts first.
     // A cache hint only: values are unaffected.
-    if (p.pf_base) {
-      const int sh = p.pf_shared ? 1 : 0;
-      const int n = min(__ldcg(p.pf_n) + sh, p.pf_max);
-      const long long ppe = (p.pf_span + kPfPiece - 1) / kPfPiece;
-      const long long pieces = (long long)n * ppe;
-      for (long long i = blockIdx.x + (long long)gridDim.x * lane; i < pieces;
-           i += (long long)gridDim.x * 32) {
-        const int j = (int)(i / ppe);
-        const long long q = (i - (long long)j * ppe) * kPfPiece;
-        const uint8_t* src = (j < sh) ? p.pf_shared
-                                      : p.pf_base + (size_t)__ldcg(p.pf_list + j - sh) * p.pf_xb;
-        const uint32_t bytes = (uint32_t)min((long long)kPfPiece, p.pf_span - q);
-        prefetch_l2_bulk(src + q, bytes);
-      }
-    }
+    issue_l2_prefetch(p.pf, blockIdx.x + (long long)gridDim.x * lane, (long long)gridDim.x * 32);
   } else if (warp == 1 && lane == 0) {
     // ===================== MMA issuer (one thread) =====================
     int stage = 0, islot = 0, acc = 0;

@@ -67,6 +67,38 @@ struct RouteInfo {
 
 constexpr int kRouteEpMax = 8;  // == kEpMaxWorld (ep.cuh)
 
+// NEXT-3 cross-layer L2 prefetch of the next layer's likely experts (base == nullptr: off):
+// that layer's hit experts at its previous step, in the order its FFN claims them (the shared
+// expert first, then ascending id), `span` bytes of each from its start (the gate/up rows).
+// A cache hint only: values are unaffected.
+constexpr int kPfPiece = 64 * 1024;  // bytes per L2 bulk prefetch
+struct L2Prefetch {
+  const uint8_t* base;    // next layer's packed experts (device_all)
+  const int* list;        // next layer's experts ranked at its previous step
+  const int* n;           // number of ranked (hit) experts
+  int max;                // budget in experts
+  long long xb;           // bytes per packed expert
+  long long span;         // bytes prefetched per expert (<= xb)
+  const uint8_t* shared;  // nullable: next layer's shared expert (prefetched first)
+  long long first;        // pieces [first, max * pieces per expert) of the ranked byte range
+};
+// Issuer `who` of `nwho` takes pieces who, who + nwho, ... of the byte range (the first-claimed
+// experts are covered by the lowest issuers first).
+__device__ __forceinline__ void issue_l2_prefetch(const L2Prefetch& f, long long who, long long nwho) {
+  if (!f.base) return;
+  const int sh = f.shared ? 1 : 0;
+  const int n = min(__ldcg(f.n) + sh, f.max);
+  const long long ppe = (f.span + kPfPiece - 1) / kPfPiece;
+  const long long pieces = (long long)n * ppe;
+  for (long long i = f.first + who; i < pieces; i += nwho) {
+    const int j = (int)(i / ppe);
+    const long long q = (i - (long long)j * ppe) * kPfPiece;
+    const uint8_t* src = (j < sh) ? f.shared : f.base + (size_t)__ldcg(f.list + j - sh) * f.xb;
+    const uint32_t bytes = (uint32_t)min((long long)kPfPiece, f.span - q);
+    prefetch_l2_bulk(src + q, bytes);
+  }
+}
+
 struct RouteParams {
   const void* x;        // [N,H] caller's block hidden states
   const void* wr;       // [E,H] router
@@ -769,7 +801,8 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            const int* __restrict__ par, int E,
                                                            T* __restrict__ out, int N, int k,
                                                            int H, int shared,
-                                                           unsigned long long* trace) {
+                                                           unsigned long long* trace,
+                                                           const __grid_constant__ L2Prefetch pf) {
   extern __shared__ int s_off[];  // [E] (dynamic: the CTA must fit beside a resident FFN CTA)
   __shared__ int s_scratch[33];
   const int n = blockIdx.x, lane = threadIdx.x & 31;
@@ -809,7 +842,11 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
     acc.z = fmaf(g, v.z, acc.z);
     acc.w = fmaf(g, v.w, acc.w);
   }
-  if (!valid) return;
+  if (!valid) {
+    issue_l2_prefetch(pf, (long long)(blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x,
+                      (long long)gridDim.x * gridDim.y * blockDim.x);
+    return;
+  }
   if (shared) {
     const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(N * k + n) * H + c));
     acc.x += v.x;
@@ -828,6 +865,10 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
     *reinterpret_cast<float4*>(o) = acc;
   }
   if (trace && threadIdx.x == 0) atomicMax(trace + 1, globaltimer_ns());  // debug: latest end
+  // NEXT-3: the FFN has finished streaming, so the next layer's likely experts are pulled
+  // into L2 now, while this combine and the next routing leave HBM idle
+  issue_l2_prefetch(pf, (long long)(blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x,
+                    (long long)gridDim.x * gridDim.y * blockDim.x);
 }
 
 }  // namespace tide

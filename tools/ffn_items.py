@@ -70,3 +70,26 @@ if len(dep):
 grid = np.arange(0, us(ct[:, 3].max()) + 1, 1.0)
 busy = [(np.array(first_claim) <= x).sum() - (us(ct[:, 2]) < x).sum() for x in grid]
 print("  CTAs issuing (per 4 us):", " ".join(str(int(b)) for b in busy[::4]))
+# aggregate weight-stream rate over time: each item's bytes spread evenly over claim -> next
+# claim of its CTA (phase 1: gate + up tiles, 2 x 128 rows x H; phase 2: 128 down rows x F)
+eb = 2 if shape.dtype == "bf16" else 4
+b_item = {0: 2 * 128 * H * eb, 1: 128 * F * eb}
+bins = np.zeros(int(us(ct[:, 3].max())) + 2)
+tot = 0.0
+for c in range(nsm):
+    n = int(ct[c, 4])
+    rows = it[c, :min(n, 64)]
+    for i, (tc, meta, td, ti) in enumerate(rows):
+        kind = int(meta) >> 32
+        nxt = rows[i + 1, 0] if i + 1 < len(rows) else ct[c, 2]
+        a, b = us(tc), us(nxt)
+        if b <= a:
+            continue
+        tot += b_item[kind]
+        rate = b_item[kind] / (b - a)
+        for x in range(int(a), int(b) + 1):
+            lo, hi = max(a, x), min(b, x + 1)
+            if hi > lo:
+                bins[x] += rate * (hi - lo)
+print(f"  weight bytes traced {tot / 1e6:.1f} MB; stream rate per 2 us (TB/s):")
+print("   ", " ".join(f"{(bins[i] + bins[i + 1]) / 2e6:.2f}" for i in range(0, len(bins) - 1, 2)))
