@@ -48,7 +48,8 @@ FLASH = Shape("flash", 256, 8, 4096, 1024, 32, 32)
 SWEEP = Shape("sweep", 256, 8, 2048, 512, 20, 256, shared_expert=True)
 SHAPES = {s.name: s for s in (TOY, MINI, FLASH, SWEEP)}
 
-# calibrated temporal-routing constants (re-checked in tests/test_gen.py)
+# calibrated temporal-routing constants (the statistics they reproduce are pinned
+# in tests/test_next_rows.py::test_generator_matches_paper_routing_statistics)
 ALPHA, SKEW, A0 = 0.99, 0.5, 0.8
 
 
