@@ -301,6 +301,7 @@ static void preload_ep_p2p_kernels(const tide_ctx* c) {
     case 16: touch(tide_route_kernel<TT, 16>); break;       \
     default: touch(tide_route_kernel<TT, 32>); break;       \
   }
+  touch(tide_book_kernel);  // the side-stream placement kernel of the EP step
   if (c->bf16) {
     TOUCH_ROUTE(__nv_bfloat16)
     touch(tide_ffn_kernel<__nv_bfloat16, true>);

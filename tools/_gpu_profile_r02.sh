@@ -33,3 +33,8 @@ for c in mini:640 sweep:640 flash1:256; do
   python tools/ffn_traffic.py --config $cfg --join $O/ffn_$cfg.csv --algo $O/ffn_${cfg}_algo.json
 done
 cp profiles/ffn_traffic.json $O/ffn_traffic.json
+# route / layer timelines and the FFN stream-rate timeline (kernel %globaltimer traces)
+timeout 300 python tools/route_trace.py mini > $O/route_trace_mini.txt 2>&1
+timeout 300 python tools/timeline.py mini > $O/timeline_mini.txt 2>&1
+timeout 300 python tools/ffn_items.py mini 12 > $O/ffn_items_mini.txt 2>&1
+echo traces rc=$?
