@@ -772,10 +772,16 @@ def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full
     y_out = sum(allc[src][rank] for src in range(world) if src != rank) * H * 4 / layer_steps
     y_in = sum(cnt[d] for d in range(world) if d != rank) * H * 4 / layer_steps
     if p2p:
-        disp = peers * (N * H * 2 + N * k * 8 + 4)
-        out_b, in_b = disp + y_out + peers * El * 4, disp + y_in + peers * El * 4
-        how = ("kernel peer stores: X rows + top-k/gates to every peer (router), pair y rows "
-               "to their token's rank (FFN epilogue), local counts to every peer")
+        # router: X rows to every peer + each remote pair's list append at its owner (a 4-byte
+        # atomic and two 4-byte stores); FFN epilogue: y rows back to their token's rank
+        app_out = sum(cnt[d] for d in range(world) if d != rank) * 12 / layer_steps
+        app_in = sum(allc[src][rank] for src in range(world) if src != rank) * 12 / layer_steps
+        disp = peers * (N * H * 2 + 4)
+        out_b = disp + app_out + y_out + peers * El * 4
+        in_b = disp + app_in + y_in + peers * El * 4
+        how = ("kernel peer stores: X rows to every peer and each pair's list append at its "
+               "expert's owner (router), pair y rows to their token's rank (FFN epilogue), "
+               "local counts to every peer")
     else:
         out_b = in_b = peers * (N * (H * 2 + k * 8) + N * H * 4 + El * 4)
         how = ("NCCL: all-gather of [x | top-k | gates] (max_tokens rows per rank), all-to-all "
