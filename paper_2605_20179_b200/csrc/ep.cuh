@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(128) tide_ep_final_p2p_kernel(
   const int par = __ldcg(par_word);
   const int n = blockIdx.x, lane = threadIdx.x & 31;
   if (n >= N && !(n == 0 && blockIdx.y == 0)) return;
-  if (!ep_wait_all(ctr + 2 + par, target, ctr + 4)) return;
+  // world 1 (target 0): the FFN grid this kernel waited on above is the only producer
+  if (target > 0 && !ep_wait_all(ctr + 2 + par, target, ctr + 4)) return;
   if (n == 0 && blockIdx.y == 0) {
     const int* hits = reinterpret_cast<const int*>(sym + lay.hits_all);
     for (int i = threadIdx.x; i < E; i += blockDim.x) hit_counts[i] = __ldcg(hits + i);

@@ -524,11 +524,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1)
       reinterpret_cast<int*>(p.ep_base[dst] + p.ep_off_hits)[p.ep_e0 + e] = __ldcg(cnt + e);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (p.ep_P > 1)
-        fence_release_sys();
-      else
-        fence_acq_rel_gpu();
+    if (threadIdx.x == 0 && p.ep_P > 1) {  // world 1: the final kernel's wait on this grid
+      fence_release_sys();
       for (int dst = 0; dst < p.ep_P; ++dst)
         red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + 2 + par, 1u);
     }

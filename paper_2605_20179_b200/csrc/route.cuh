@@ -435,20 +435,17 @@ __device__ __forceinline__ void route_tail(const RouteParams& p, int* cnt, int p
     if (old == (int)gridDim.y - 1) {
       *p.g_done = 0;
       *p.par = par ^ 1;  // consumers (FFN, book) read this step's counts at cnt2[par ^ 1]
-      if (p.ep_P) {  // every CTA's peer stores precede this point (each CTA released them
-                     // itself at world > 1; the g_cnt / g_done chains acquired them here):
-                     // one release fence (system scope when a peer is another GPU), then
-                     // the arrivals
-        if (p.ep_P > 1)
-          fence_release_sys();
-        else
-          fence_acq_rel_gpu();
+      if (p.ep_P > 1) {  // every CTA's peer stores precede this point (each CTA released
+                         // them itself; the g_cnt / g_done chains acquired them here): one
+                         // system-scope release fence, then the arrivals.  World 1 has no
+                         // peer: the FFN's wait on this grid orders everything (stream order)
+        fence_release_sys();
         for (int dst = 0; dst < p.ep_P; ++dst)
           red_relaxed_sys_add_u32(reinterpret_cast<unsigned*>(p.ep_base[dst] + p.ep_off_ctr) + (par ^ 1), 1u);
       }
     }
   }
-  if (p.ep_lists) route_ep_wait(p, par, s_flag);
+  if (p.ep_lists && p.ep_P > 1) route_ep_wait(p, par, s_flag);
 }
 
 // Peer-memory EP dispatch of X: CTA (bx, by) stores uint4 columns [bx*per, (bx+1)*per) of

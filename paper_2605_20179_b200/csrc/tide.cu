@@ -1604,7 +1604,8 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   if (c->p2p) {  // the FFN stored every pair's y at its owner and arrived (ffn.cuh)
     if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
     const dim3 grid(std::max(N, 1), nY);
-    const unsigned tgt = (unsigned)c->ep_arrivals;  // one arrival per FFN CTA of every rank
+    // one arrival per FFN CTA of every rank; none at world 1 (stream order suffices)
+    const unsigned tgt = c->world > 1 ? (unsigned)c->ep_arrivals : 0u;
     if (c->bf16)
       CU_TRY(launch_pdl(tide_ep_final_p2p_kernel<__nv_bfloat16>, grid, dim3(128), 0, st, c->sym,
                         c->lay, (const int*)c->cnt_par, tgt, (const float*)c->gates,
