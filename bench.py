@@ -489,6 +489,30 @@ class Stack:
                 acc["launches"] += r["ffn_launches"]
         return acc
 
+    def routing_stats(self, B=64):
+        """the routing the synthetic inputs produce, measured on the GPU's own
+        routing over one block of layer 0 with the NEXT-4 analytics kernel (tide_trace_stats):
+        mean adjacent-step and lag-5 cosine of the hit-count vectors, unique
+        experts per step, mean Eq. 4 drift of the top-B placement."""
+        s, L = self.s, self.layers[0]
+        T = s.steps
+        counts = torch.empty(T, s.num_experts, dtype=torch.int32, device=self.dev)
+        self.reset()
+        for t in range(T):
+            self.layer_step(L, t)
+            counts[t].copy_(L["hits"])
+        sim, uq, dr = self.tide.trace_stats(counts, min(B, s.num_experts))
+        torch.cuda.synchronize()
+        sim = sim.cpu().numpy()
+        uq = uq.cpu().numpy()
+        return {"adjacent_cosine": round(float(np.mean([sim[t, t + 1] for t in range(T - 1)])), 4),
+                "lag5_cosine": round(float(np.mean([sim[t, t + 5] for t in range(T - 5)])), 4),
+                "unique_experts_per_step": [int(v) for v in uq],
+                "drift_top%d_mean" % min(B, s.num_experts): round(float(dr.cpu().numpy().mean()), 4),
+                "paper": "adjacent 0.985 (P:200), > 0.95 at 5 steps (P:203), unique experts grow "
+                         "within a block (P:126-127)",
+                "layer": 0}
+
     def e2e(self, steps, warmup, graphs: bool):
         """Same metric through the public API with every layer-step's hidden states copied
         H2D from pinned host and its output D2H, on a copy stream that overlaps the transfers
@@ -668,6 +692,8 @@ def measure_single(args, s: g.Shape, cap: int, dev, rank=0, world=1, weights=Non
             "ffn_launches_per_layer_step": round(acc["launches"] / layer_steps, 2)}
     if full and not args.no_e2e:
         res["e2e"] = st.e2e(steps, warmup, graphs)
+    if full and not pool:
+        res["routing_stats"] = st.routing_stats()
     st.close()
     del st
     torch.cuda.empty_cache()
