@@ -96,6 +96,10 @@ def parse():
                          "(the N>1 default)")
     ap.add_argument("--nccl", action="store_true",
                     help="EP headline on the NCCL collectives instead of peer memory")
+    ap.add_argument("--strong", action="store_true",
+                    help="EP strong scaling (SURVEY 8(d) flash-EP): 8 blocks (256 tokens) in "
+                         "total per layer-step, split over the N ranks (default: one block "
+                         "per rank, weak scaling)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent per-rank stacks (no data-path collective) instead of EP")
     return ap.parse_args()
@@ -856,8 +860,14 @@ def run_tide(args, rank: int, world: int, local_rank: int, nccl_ok: bool = True)
     ep = (args.ep or world > 1) and not args.replicas
     name = args.config or ("flash" if ep and world > 1 else "mini")
     s = shape_for(name, args.layers)
+    strong = bool(args.strong and ep)
+    if strong:  # 8 blocks in total per layer-step, split over the ranks
+        s = g.Shape(s.name, s.num_experts, s.top_k, s.hidden, s.ffn, s.layers,
+                    max(1, 8 * 32 // world), s.steps, s.interval, s.capacity, s.dtype,
+                    s.shared_expert)
     base = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: tidegen seeded weights (U(+-sqrt(3/fan_in)), bf16) and " +
                     ("calibrated temporal block routing (alpha=0.99, skew=0.5, a0=0.8)"
