@@ -41,7 +41,7 @@ def test_bench_single_process_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
-@pytest.mark.parametrize("extra", [["--replicas"], []])
+@pytest.mark.parametrize("extra", [["--replicas"], [], ["--strong"]])
 def test_bench_torchrun_two_ranks_one_gpu(extra):
     """torchrun x2 in the one-GPU test mode: replicas, and the N>1 default (flash-shaped
     expert parallelism over peer memory, NVLink accounting) on a 2-layer stack."""
@@ -53,8 +53,11 @@ def test_bench_torchrun_two_ranks_one_gpu(extra):
     assert r.returncode == 0, r.stderr[-2000:]
     d = _line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0
-    ep = not extra
+    ep = "--replicas" not in extra
     assert ("expert parallel x2" in d["config"]["parallelism"]) == ep
+    assert d["scaling"] == ("strong" if "--strong" in extra else "weak")
+    if "--strong" in extra:  # 8 blocks in total, split over the 2 ranks
+        assert d["config"]["tokens_per_layer_step_per_rank"] == 128
     if ep:
         assert "flash" in d["config"]["workload"] and d["nvlink"]["bytes_out_per_layer_step"] > 0
         assert 0 < d["roofline"]["frac"] < 1.2
