@@ -269,6 +269,62 @@ def gather_over_ranks(vec: list, world: int, dev) -> list:
     return [o.cpu().tolist() for o in out]
 
 
+def gather_tensor(t: torch.Tensor, world: int, dev) -> list:
+    """All ranks' copies of a same-shape device tensor (NCCL: on the device; gloo: via host)."""
+    if world == 1:
+        return [t]
+    gloo = torch.distributed.get_backend() == "gloo"
+    src = t.contiguous().cpu() if gloo else t.contiguous()
+    out = [torch.empty_like(src) for _ in range(world)]
+    torch.distributed.all_gather(out, src)
+    return [o.to(dev) for o in out]
+
+
+def ep_check(st, args, s: g.Shape, dev, rank: int, world: int, p2p: bool) -> dict:
+    """Correctness of the measured EP configuration on this machine, checked on the GPU: one
+    EP layer-step (layer 0, t = 0) on every rank's tokens against the single-device step over
+    all ranks' tokens, computed on rank 0 with every expert of the layer (DESIGN 8: the
+    peer-memory EP output is bitwise equal to it for any world size; the NCCL path sums the
+    ranks' partials in rank order, so it is compared within the 2e-2 output tolerance)."""
+    tide = st.tide
+    L = st.layers[0]
+    st.reset()
+    st.layer_step(L, 0)
+    torch.cuda.synchronize()
+    xs = gather_tensor(L["x"][0], world, dev)
+    outs = gather_tensor(L["out"], world, dev)
+    res = torch.zeros(3, dtype=torch.float64, device=dev)
+    if rank == 0:
+        E, k, H, F = s.num_experts, s.top_k, s.hidden, s.ffn
+        x = torch.cat(xs)
+        desc = tide.make_desc(E, k, H, F, x.shape[0], tide.TIDE_BF16, shared_expert=s.shared_expert)
+        _, w, shared = gen_layer(args, s, 0, dev, desc)  # every expert of layer 0
+        ctx = tide.Context(desc, E, 16, dev.index)
+        pl = torch.zeros(E, dtype=torch.uint8, device=dev)
+        r = ctx.moe_step(x, L["router"], device_all=w, shared_w=shared, placement=pl, step=0,
+                         interval=args.interval)
+        torch.cuda.synchronize()
+        ep_out = torch.cat(outs)
+        diff = (r.out.view(torch.int16) != ep_out.view(torch.int16)).sum()
+        ref = r.out.float()
+        rel = (ep_out.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30)
+        res[0], res[1], res[2] = float(diff.item()), float(rel.item()), float(x.shape[0])
+        ctx.close()
+        del w, shared, ctx, r
+        torch.cuda.empty_cache()
+    if world > 1:
+        gloo = torch.distributed.get_backend() == "gloo"
+        rr = res.cpu() if gloo else res
+        torch.distributed.broadcast(rr, 0)
+        res = rr
+    mism, rel, ntok = int(res[0].item()), float(res[1].item()), int(res[2].item())
+    return {"layer": 0, "step": 0, "tokens": ntok, "mismatched_elements": mism,
+            "bitwise_equal_single_device": mism == 0, "max_rel_err": rel,
+            "pass": (mism == 0) if p2p else rel < 2e-2,
+            "how": "rank 0 recomputes the layer-step over all ranks' tokens on one GPU with "
+                   "every expert and compares the gathered EP outputs"}
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -788,6 +844,7 @@ def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full
     tot, launches = phase_sums(phases)
     layer_steps = steps * s.layers
     value = N * layer_steps * world / (ms / 1e3)
+    check = ep_check(st, args, s, dev, rank, world, p2p) if full else None
     acc = st.stats_replay(steps, warmup)
     pk = peaks()
     peak = pk.get("hbm_gbs", 6650.0)
@@ -843,6 +900,7 @@ def measure_ep(args, s: g.Shape, dev, rank, world, p2p: bool, weights=None, full
            "phases_us_per_layer_step": {kk: round(1e3 * v / layer_steps, 2) for kk, v in tot.items()}}
     if full:
         res["clocks"] = clocks
+        res["ep_check"] = check
         res["step_split"] = st.step_split(steps, warmup)
         if not args.no_e2e:
             res["e2e"] = st.e2e(steps, warmup, graphs)

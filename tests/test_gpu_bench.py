@@ -60,6 +60,8 @@ def test_bench_torchrun_two_ranks_one_gpu(extra):
         assert d["config"]["tokens_per_layer_step_per_rank"] == 128
     if ep:
         assert "flash" in d["config"]["workload"] and d["nvlink"]["bytes_out_per_layer_step"] > 0
+        # the run's own check: EP output over both ranks' tokens == the single-device step
+        assert d["ep_check"]["pass"] and d["ep_check"]["bitwise_equal_single_device"], d["ep_check"]
         assert 0 < d["roofline"]["frac"] < 1.2
 
 
