@@ -798,8 +798,7 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
                                                            const int* __restrict__ par, int E,
                                                            T* __restrict__ out, int N, int k,
                                                            int H, int shared,
-                                                           unsigned long long* trace,
-                                                           const __grid_constant__ L2Prefetch pf) {
+                                                           unsigned long long* trace) {
   extern __shared__ int s_off[];  // [E] (dynamic: the CTA must fit beside a resident FFN CTA)
   __shared__ int s_scratch[33];
   const int n = blockIdx.x, lane = threadIdx.x & 31;
@@ -839,11 +838,7 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
     acc.z = fmaf(g, v.z, acc.z);
     acc.w = fmaf(g, v.w, acc.w);
   }
-  if (!valid) {
-    issue_l2_prefetch(pf, (long long)(blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x,
-                      (long long)gridDim.x * gridDim.y * blockDim.x);
-    return;
-  }
+  if (!valid) return;
   if (shared) {
     const float4 v = __ldcg(reinterpret_cast<const float4*>(y + (size_t)(N * k + n) * H + c));
     acc.x += v.x;
@@ -862,10 +857,6 @@ __global__ void __launch_bounds__(128) tide_combine_kernel(const float* __restri
     *reinterpret_cast<float4*>(o) = acc;
   }
   if (trace && threadIdx.x == 0) atomicMax(trace + 1, globaltimer_ns());  // debug: latest end
-  // NEXT-3: the FFN has finished streaming, so the next layer's likely experts are pulled
-  // into L2 now, while this combine and the next routing leave HBM idle
-  issue_l2_prefetch(pf, (long long)(blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x,
-                    (long long)gridDim.x * gridDim.y * blockDim.x);
 }
 
 }  // namespace tide

@@ -161,7 +161,6 @@ struct tide_ctx {
   bool knob_route_ksplit1 = false;  // TIDE_ROUTE_KSPLIT1=1: one router CTA per 16 x 8 tile
   bool knob_pf_by_hits = false;    // TIDE_PF_BY_HITS=1: prefetch ranked by hits, no shared expert
   bool knob_pf_whole = false;      // TIDE_PF_WHOLE_EXPERT=1: prefetch whole experts (not gate/up)
-  int knob_pf_at = 1;              // TIDE_PF_AT: L2 prefetch issued by 1 the FFN tail, 2 the combine, 3 both
   int64_t pf_self_bytes = -1;      // own-layer prefetch before the FFN's routing wait (-1: half
                                    // the previous layer's tail budget; TIDE_PF_SELF_MB overrides)
   int64_t pf_prev_budget = 0;      // budget of the context whose FFN tail prefetches this layer
@@ -517,7 +516,6 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->knob_route_ksplit1 = getenv("TIDE_ROUTE_KSPLIT1") != nullptr;
   c->knob_pf_by_hits = getenv("TIDE_PF_BY_HITS") != nullptr;
   c->knob_pf_whole = getenv("TIDE_PF_WHOLE_EXPERT") != nullptr;
-  if (const char* v = getenv("TIDE_PF_AT")) c->knob_pf_at = std::max(1, std::min(3, atoi(v)));
   if (const char* v = getenv("TIDE_PF_SELF_MB")) c->pf_self_bytes = (int64_t)(atof(v) * 1048576.0);
   if (const char* v = getenv("TIDE_H2D_PF_MIN_HITS")) c->pf_min_hits = std::max(1, atoi(v));
   *out = c;
@@ -852,8 +850,8 @@ static tide_status ensure_pool(tide_ctx* c) {
 // build mode: cnt != nullptr (every CTA derives the work list from the counts);
 // global mode: entries/n_entries (host-built staged chunk).
 // NEXT-3 cross-layer L2 prefetch of the next layer's likely experts (tide_ctx_set_prefetch);
-// all-null when off.  Issued by the FFN's CTAs as they run out of work and/or by the combine
-// after the FFN has finished (TIDE_PF_AT, A/B knob).
+// all-null when off.  Issued by the FFN's CTAs as they run out of work (a combine-issued
+// variant was measured and removed, DESIGN 11).
 static L2Prefetch l2_prefetch_of(const tide_ctx* c) {
   L2Prefetch f{};
   if (!(c->pf_next && c->pf_weights && c->pf_max > 0)) return f;
@@ -884,7 +882,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   p.map_h = c->map_h;
   p.cnt = cnt;
   p.par = par;
-  p.pf = (prefetch && (c->knob_pf_at & 1)) ? l2_prefetch_of(c) : L2Prefetch{};
+  p.pf = prefetch ? l2_prefetch_of(c) : L2Prefetch{};
   p.pf_self = L2Prefetch{};
   const int64_t self_bytes = c->pf_self_bytes >= 0 ? c->pf_self_bytes : c->pf_prev_budget / 2;
   if (prefetch && self_bytes > 0 && c->pf_target && cnt && !slot_of && c->map_src) {
@@ -898,7 +896,7 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
     f.span = c->knob_pf_whole ? f.xb : f.xb / 3 * 2;
     f.shared = c->knob_pf_by_hits ? nullptr : static_cast<const uint8_t*>(c->map_shared_src);
     const long long ppe = (f.span + kPfPiece - 1) / kPfPiece;
-    const int64_t prev = (c->knob_pf_at & 1) ? c->pf_prev_budget : 0;  // the tail's range
+    const int64_t prev = c->pf_prev_budget;  // the range the previous layer's FFN tail covers
     const int done_e = prev > 0 ? (int)std::min<int64_t>(c->E + 1, prev / f.span) : 0;
     f.first = (long long)done_e * ppe;
     f.max = (int)std::min<int64_t>(c->E + 1, (prev + self_bytes) / f.span);
@@ -1467,17 +1465,16 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
     const dim3 grid(N, (H + 511) / 512);
     unsigned long long* ctr =  // debug: [6] latest start, [7] latest end in CTA 0's FFN record
         (dbg && dbg->ffn_trace) ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) + 6 : nullptr;
-    const L2Prefetch cpf = (!pool_mode && (c->knob_pf_at & 2)) ? l2_prefetch_of(c) : L2Prefetch{};
     if (c->bf16)
       CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), sizeof(int) * E, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
-                        static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr, cpf));
+                        static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr));
     else
       CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), sizeof(int) * E, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
-                        static_cast<float*>(out), N, k, H, shared ? 1 : 0, ctr, cpf));
+                        static_cast<float*>(out), N, k, H, shared ? 1 : 0, ctr));
     c->launches++;
   }
   if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4/a5 outputs
