@@ -1,0 +1,12 @@
+#!/bin/bash
+# round-2 closing refresh on one B200: GPU tests + smoke + every bench line, the profile set
+# (launch lists, ncu full route/FFN, DRAM traffic joins, traces), sanitizers, the tau x C sweep
+bash tools/_gpu_final.sh > gpurun_out/final.log 2>&1
+echo "== final"; tail -32 gpurun_out/final.log
+bash tools/_gpu_profile_r02.sh > gpurun_out/profile.log 2>&1
+echo "== profile"; tail -10 gpurun_out/profile.log | cut -c1-200
+rm -f gpurun_out/sanitizer/summary.txt
+bash tools/_gpu_sanitize.sh > /dev/null 2>&1
+echo "== sanitizer"; cut -c1-150 gpurun_out/sanitizer/summary.txt
+mkdir -p gpurun_out/r02
+timeout 1500 python tools/sweep_interval.py --layers 2 --out gpurun_out/r02/sweep_interval.json > gpurun_out/r02/sweep_interval.log 2>&1; echo "sweep rc=$?"
