@@ -40,7 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nccl_inc, nccl_lib = nccl_dirs()
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-o", LIB,
+    extra = os.environ.get("TIDE_NVCC_EXTRA", "").split()  # A/B builds only (tools/_gpu_ab_vars.sh)
+    cmd = [NVCC] + FLAGS + extra + ["-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-o", LIB,
                             os.path.join(CSRC, "tide.cu"), "-L", nccl_lib, "-l:libnccl.so.2",
                             "-Xlinker", "-rpath=" + nccl_lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
