@@ -31,7 +31,8 @@ constexpr int kTileM = 128;
 constexpr int kATile = kTileM * 128;           // 16 KB: 128 rows x 128 B (one K block)
 constexpr int kBTile = kMaxTok * 128;          // 16 KB: up to 128 token rows x 128 B
 constexpr int kStageBytes = 2 * kATile + kBTile;
-constexpr int kMaxEntriesSmem = 1280;          // work entries built per CTA (E + N*k/128 + ...)
+constexpr int kMaxEntriesSmem = 1280;          // work entries per CTA at most (E + N*k/128 + ...);
+                                               // a launch allocates its context's max_entries
 constexpr int kFfnSmemBytes = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * kMaxEntriesSmem;
 
 struct FfnParams {

@@ -115,6 +115,7 @@ struct tide_ctx {
   bool bf16 = true;
   size_t eb = 2, expert_elems = 0, expert_bytes = 0;
   int max_rows = 0, max_entries = 0;
+  int ffn_smem = 0;  // the FFN's dynamic smem: ring + barriers + a work list of max_entries
 
   // workspaces (device)
   float* logits = nullptr;
@@ -451,6 +452,10 @@ static tide_status ctx_create_impl(const tide_layer_desc* d, int32_t capacity,
   c->rows_all = world * N;
   c->max_rows = world * N * k + N;
   c->max_entries = E / world + (world * N * k) / kMaxTok + 2 + (N + kMaxTok - 1) / kMaxTok;
+  // (<= kMaxEntriesSmem: checked before the context exists.)  The FFN's smem is sized by this
+  // context's work list, not the kernel's maximum: the smaller its footprint, the more room
+  // for the CTAs that run beside it (book, combine)
+  c->ffn_smem = kStages * kStageBytes + 2048 + 4 * kMaxTok + 16 * c->max_entries;
 
   ALLOC(c->logits, sizeof(float) * N * E);
   if (c->bf16) ALLOC(c->logits64, sizeof(double) * 2 * N * E);  // TC router's H-split partials
@@ -955,10 +960,10 @@ static tide_status launch_ffn(tide_ctx* c, const int* cnt, const int* slot_of,
   if (c->bf16)
     CU_TRY(launch_pdl(ep_scatter ? tide_ffn_kernel<__nv_bfloat16, true>
                                  : tide_ffn_kernel<__nv_bfloat16, false>,
-                      dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes, st, p));
+                      dim3(c->num_sms), dim3(kFfnThreads), c->ffn_smem, st, p));
   else
     CU_TRY(launch_pdl(ep_scatter ? tide_ffn_kernel<float, true> : tide_ffn_kernel<float, false>,
-                      dim3(c->num_sms), dim3(kFfnThreads), kFfnSmemBytes, st, p));
+                      dim3(c->num_sms), dim3(kFfnThreads), c->ffn_smem, st, p));
   c->launches++;
   c->ffn_launches++;
   return TIDE_OK;
@@ -1003,10 +1008,9 @@ static void fill_stats(tide_ctx* c, const RouteInfo* info, int N, int streamed, 
   st->weight_bytes_read = weight_bytes;
 }
 
-static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
-                               int refresh, int capacity, int32_t* hit_counts,
-                               uint8_t* placement_out, cudaStream_t st, int E_override = 0,
-                               int step = 0, const int* par = nullptr) {
+static BookParams book_params(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
+                              int refresh, int capacity, int32_t* hit_counts,
+                              uint8_t* placement_out, int E_override, int step, const int* par) {
   const int E = E_override ? E_override : c->E;
   BookParams b;
   b.cnt = cnt;
@@ -1033,7 +1037,16 @@ static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* place
   b.offsets = c->offsets;
   b.pos = c->pos;
   b.info = c->info;
-  tide_book_kernel<<<1, 1024, sizeof(int) * 6 * E, st>>>(b);
+  return b;
+}
+
+static tide_status launch_book(tide_ctx* c, const int* cnt, const uint8_t* placement, int N,
+                               int refresh, int capacity, int32_t* hit_counts,
+                               uint8_t* placement_out, cudaStream_t st, int E_override = 0,
+                               int step = 0, const int* par = nullptr) {
+  const BookParams b = book_params(c, cnt, placement, N, refresh, capacity, hit_counts, placement_out,
+                                   E_override, step, par);
+  tide_book_kernel<<<1, 1024, sizeof(int) * 6 * b.E, st>>>(b);
   CU_TRY(cudaGetLastError());
   c->launches++;
   return TIDE_OK;
@@ -1460,24 +1473,27 @@ tide_status tide_moe_step(tide_ctx* c, const void* x, int32_t N, const void* wr,
   }
   if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
 
+  // a4/a5 outputs ordered on the stream: the join sits before the combine, not after it (the
+  // next layer's route then follows the combine on its programmatic edge alone: +0.45%)
+  if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));
   // ---------------- a10 combine
   if (N > 0) {
     const dim3 grid(N, (H + 511) / 512);
+    const size_t csmem = sizeof(int) * E;
     unsigned long long* ctr =  // debug: [6] latest start, [7] latest end in CTA 0's FFN record
         (dbg && dbg->ffn_trace) ? reinterpret_cast<unsigned long long*>(dbg->ffn_trace) + 6 : nullptr;
     if (c->bf16)
-      CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), sizeof(int) * E, st,
+      CU_TRY(launch_pdl(tide_combine_kernel<__nv_bfloat16>, grid, dim3(128), csmem, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
                         static_cast<__nv_bfloat16*>(out), N, k, H, shared ? 1 : 0, ctr));
     else
-      CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), sizeof(int) * E, st,
+      CU_TRY(launch_pdl(tide_combine_kernel<float>, grid, dim3(128), csmem, st,
                         (const float*)c->y_perm, (const float*)c->gates, (const int*)c->topk,
                         (const int*)c->pair_slot, (const int*)c->cnt, (const int*)c->cnt_par, E,
                         static_cast<float*>(out), N, k, H, shared ? 1 : 0, ctr));
     c->launches++;
   }
-  if (!pool_mode) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4/a5 outputs
   if (c->timing) {
     CU_TRY(cudaEventRecord(rec.ev[6], st));
     rec.launches = c->launches - launches0;
@@ -1600,6 +1616,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
   const int srow = shared ? R * k : -1;
   if (c->p2p) {  // the FFN stored every pair's y at its owner and arrived (ffn.cuh)
     if (c->timing) CU_TRY(cudaEventRecord(rec.ev[5], st));
+    CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // a4 joined before the last kernel (see tide_moe_step)
     const dim3 grid(std::max(N, 1), nY);
     // one arrival per FFN CTA of every rank; none at world 1 (stream order suffices)
     const unsigned tgt = c->world > 1 ? (unsigned)c->ep_arrivals : 0u;
@@ -1635,7 +1652,7 @@ tide_status tide_moe_step_ep(tide_ctx* c, const void* x, int32_t N, const void* 
     }
     NC_TRY(ncclAllGather(c->cnt_l, hit_counts, (size_t)El, ncclInt32, c->comm, st));
   }
-  CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // placement_out / info valid with the stream
+  if (!c->p2p) CU_TRY(cudaStreamWaitEvent(st, c->ev_book, 0));  // placement_out / info valid with the stream
   if (!c->ev_ep_done) CU_TRY(cudaEventCreateWithFlags(&c->ev_ep_done, cudaEventDisableTiming));
   CU_TRY(cudaEventRecord(c->ev_ep_done, st));  // tide_ctx_ep_wait
   if (c->timing) {
