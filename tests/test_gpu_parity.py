@@ -194,6 +194,24 @@ def test_repeat_runs_bitwise_identical():
     assert (a == b).all()
 
 
+def test_sweep_uniform_stress_parity_and_repeat():
+    """Uniform iid routing at the sweep shape (256 tokens, ~all 256 experts hit, two shared
+    entries): the FFN's phase-2 items wait on many entries' phase-1 counters and re-acquire
+    their 32-entry windows often (ffn.cuh).  Every token against the oracle, and three
+    repeats bitwise identical."""
+    from paper_2605_20179_b200 import tide
+    shape = g.SWEEP
+    layer = DeviceLayer(shape, 13, skew=0.0)
+    ctx = tide.Context(desc_for(shape), shape.num_experts)
+    x_np = g.block_hidden_np(shape, 13, steps=1, iid=True)[0]
+    r, ref, err, _ = _run_and_check(shape, 13, x_np, layer, ctx, np.zeros(256, np.uint8), 0, 1,
+                                    shape.num_experts)
+    assert int((r.hit_counts > 0).sum()) > 200
+    x = g.np_to_torch(x_np, "cuda")
+    outs = [_out_bytes(ctx, layer, x, np.zeros(256, np.uint8), 0, 1, 256) for _ in range(3)]
+    assert all((o == outs[0]).all() for o in outs[1:])
+
+
 def test_interval_one_and_io_model_match_oracle():
     """tau = 1 equals the per-step refresh policy, and the pinned-host I/O
     counters match the oracle's slot model (O10) step by step."""
